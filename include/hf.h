@@ -1,0 +1,169 @@
+/*
+ * hf.h — C-ABI of libhf.so, the B200 (sm_100a) implementation of the hot path
+ * of the reference package `hyperfree` (arXiv:1904.13131 re-implementation,
+ * /root/reference/pkg/src/hyperfree).  Cited as file:line below.
+ *
+ * The reference is pure Python; its "plugin boundary" is the duck-typed
+ * operator API (MatrixFreeTangent.apply/.diagonal, compute_residual,
+ * TransferOperator, restrict_solution, the Chebyshev/CG vector algebra).  Each
+ * entry point below replaces one of those calls.  INTEGRATION.md shows the
+ * ctypes binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - every call returns int status: HF_OK (0) or an HF_ERR_* code; the message
+ *    of the last failure on the calling thread is hf_last_error();
+ *  - "_dev" pointers are device (CUDA global memory) fp64 arrays; all other
+ *    pointers are host memory;
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *    hot-path calls are asynchronous on that stream, setup calls synchronise;
+ *  - vectors use the reference layout: lexicographic lattice nodes (x
+ *    fastest), DoF = node * dim + component (fespace.py:3-8);
+ *  - per-q-point arrays are SoA: field f of q-point (cell e, local q) at
+ *    f * n_qp + e * nq + q.
+ */
+#ifndef HF_H
+#define HF_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HF_API __attribute__((visibility("default")))
+#define HF_ABI_VERSION 1
+
+#define HF_OK 0
+#define HF_ERR_ARG 1
+#define HF_ERR_CUDA 2
+#define HF_ERR_UNSUPPORTED 3
+#define HF_ERR_JACOBIAN 4 /* det F <= 0 (material.py:34-40, operators.py:184-188) */
+#define HF_ERR_GEOMETRY 5 /* non-positive mapping Jacobian (mesh.py:302-306) */
+
+/* caching strategies, operators.py:72 STRATEGIES */
+#define HF_SCALAR 0
+#define HF_TENSOR2 1
+#define HF_TENSOR4 2
+
+typedef struct hf_space hf_space;       /* one discretisation level (Problem)  */
+typedef struct hf_tangent hf_tangent;   /* MatrixFreeTangent                   */
+typedef struct hf_transfer hf_transfer; /* TransferOperator                    */
+typedef struct hf_ws hf_ws;             /* reduction workspace (one per stream) */
+
+typedef struct {
+  int code;          /* HF_ERR_JACOBIAN when det F <= 0                        */
+  long long element; /* argmin element, as NonPositiveJacobian.element        */
+  int qpoint;        /* argmin quadrature point                               */
+  double det;        /* min det F                                             */
+} hf_error_info;
+
+HF_API const char* hf_last_error(void);
+HF_API int hf_abi_version(void);
+HF_API int hf_max_degree(int dim);
+
+/* ---- Problem (operators.py:83-116; build_dof_map fespace.py:125-139;
+ *      compute_geometry_cache mesh.py:290-307) -------------------------------
+ * cells[dim] per-axis cell counts of a structured box lattice (the reference
+ * builds cubes, cells[a] = n_cells_per_side); values/derivs_1d are the
+ * Basis1D tables (p+1, q) row-major (fespace.py:65-102); vertices
+ * (n_vertices, dim) lexicographic (mesh.py:157-167, may be perturbed);
+ * mu_el/lam_el per cell (operators.py:101-103); mask per DoF
+ * (ConstraintSet.mask, fespace.py:154-167).  Geometry (J^-1, JxW per q-point)
+ * is computed on the device. */
+HF_API int hf_space_create(int dim, int degree, int nq1, const int* cells, const double* values_1d,
+                           const double* derivs_1d, const double* qpoints_1d, const double* qweights_1d,
+                           const double* vertices, const double* mu_el, const double* lam_el,
+                           const unsigned char* mask, void* stream, hf_space** out);
+/* replace the constraint mask (Problem.constraints is mutable) */
+HF_API int hf_space_set_mask(hf_space* sp, const unsigned char* mask, void* stream);
+HF_API int hf_space_info(const hf_space* sp, long long* n_dofs, long long* n_el, long long* n_qp);
+/* device views of GeometryCache.jac_inv (SoA [dim*dim][n_qp]), .jxw, and the mask */
+HF_API int hf_space_pointers(const hf_space* sp, const double** jinv_dev, const double** jxw_dev,
+                             const unsigned char** mask_dev);
+/* copy the geometry into caller-owned device buffers (same SoA layout) */
+HF_API int hf_space_geometry_copy(const hf_space* sp, double* jinv_dev, double* jxw_dev, void* stream);
+HF_API int hf_space_destroy(hf_space* sp);
+
+/* ---- jacobian_range (operators.py:192-196) ---- */
+HF_API int hf_jacobian_range(hf_space* sp, const double* u_dev, void* stream, double* jmin, double* jmax,
+                             long long* argmin_element, int* argmin_qpoint);
+
+/* ---- MatrixFreeTangent (operators.py:319-417) -------------------------------
+ * create == __init__ + build_cache (292-311); fails with HF_ERR_JACOBIAN and a
+ * filled hf_error_info when det F <= 0 (the NonPositiveJacobian path). */
+HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev, void* stream, hf_tangent** out,
+                             hf_error_info* err);
+/* .apply (331-339): y = A x with zero-in / identity-out constrained handling */
+HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream);
+/* same, but a no-op while *skip_dev != 0 (device-side early exit for graphs) */
+HF_API int hf_tangent_apply_flagged(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                    void* stream);
+/* accumulate only: y += A_loc x over the cells, constrained rows dropped
+ * (_local_apply + distribute_local_to_global, 341-393 / fespace.py:307-324) */
+HF_API int hf_tangent_apply_raw(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                void* stream);
+/* .diagonal (395-410) */
+HF_API int hf_tangent_diagonal(hf_tangent* op, double* diag_dev, void* stream);
+/* .storage_bytes (412-417), cache.payload_scalars_per_qpoint / payload_nbytes (244-289) */
+HF_API int hf_tangent_storage(const hf_tangent* op, long long* storage_bytes, int* payload_scalars,
+                              long long* payload_bytes);
+HF_API int hf_tangent_destroy(hf_tangent* op);
+
+/* ---- compute_residual (operators.py:205-224) ----
+ * traction: host double[dim] or NULL; surf_w_dev: top_surface_weights
+ * (operators.py:129-167) per lattice node, required with a traction. */
+HF_API int hf_residual(hf_space* sp, const double* u_dev, const double* traction, const double* surf_w_dev,
+                       double* out_dev, void* stream, hf_error_info* err);
+
+/* ---- TransferOperator (multigrid.py:27-73) ----
+ * interp_1d[a]: host (n_fine_a, n_coarse_a) row-major 1D interpolation matrix
+ * of axis a (_interpolation_matrix_1d, multigrid.py:58-73).
+ * mode: 0 plain; 1 constrained outputs zeroed (v_cycle r_c[mask]=0,
+ * multigrid.py:327); 2 out += result with constrained rows dropped
+ * (x += corr after corr[mask]=0, multigrid.py:329-331). */
+HF_API int hf_transfer_create(const hf_space* coarse, const hf_space* fine, const double* const* interp_1d,
+                              hf_transfer** out);
+HF_API int hf_prolong(hf_transfer* t, const double* xc_dev, double* xf_dev, int mode, void* stream);
+HF_API int hf_restrict(hf_transfer* t, const double* rf_dev, double* rc_dev, int mode, void* stream);
+HF_API int hf_transfer_destroy(hf_transfer* t);
+/* restrict_solution, one level (multigrid.py:76-92); keep_constrained != 0
+ * keeps prescribed (non-zero Dirichlet) values */
+HF_API int hf_inject(const hf_space* coarse, const hf_space* fine, const double* uf_dev, double* uc_dev,
+                     int keep_constrained, void* stream);
+
+/* ---- vector algebra of chebyshev_apply / coarse_solve / cg / Lanczos
+ *      (multigrid.py:112-306, solver.py:34-76) ---- */
+HF_API int hf_ws_create(hf_ws** out);
+HF_API int hf_ws_destroy(hf_ws* w);
+/* out_dev[0] = a . b  (deterministic order) */
+HF_API int hf_dot(hf_ws* w, long long n, const double* a, const double* b, double* out_dev, const int* skip_dev,
+                  void* stream);
+/* y = mask ? (x ? x : masked_value) : 0 */
+HF_API int hf_fill_masked(long long n, double* y, const double* x, const unsigned char* mask, double masked_value,
+                          void* stream);
+/* z = inv_d (b - ax); d = first ? z/theta : cd d + cz z; x = (x_zero ? 0 : x) + d
+ * (ax == NULL means A x = 0) */
+HF_API int hf_cheb_step(long long n, double* x, double* d, const double* b, const double* ax, const double* inv_d,
+                        int first, double theta, double cd, double cz, int x_zero, const int* skip_dev, void* stream);
+/* r = b - ax; r[mask] = 0 (v_cycle, multigrid.py:324-325) */
+HF_API int hf_resid_masked(long long n, double* r, const double* b, const double* ax, const unsigned char* mask,
+                           void* stream);
+/* scal[out] = ||b - ax||^2; *flag = 1 if sqrt(scal[out]) <= scal[target] (coarse_solve check) */
+HF_API int hf_resnorm_check(hf_ws* w, long long n, const double* b, const double* ax, double* scal_dev, int out_idx,
+                            int target_idx, int* flag_dev, void* stream);
+/* op 0: flag |= sqrt(scal[a]) <= scal[b];  op 1: scal[b] = rel*sqrt(scal[a]), flag = (scal[a] == 0) */
+HF_API int hf_scalar_op(int op, double* scal_dev, int a, int b, double rel, int* flag_dev, void* stream);
+/* alpha = scal[irz]/scal[ipap]; x += alpha p; r -= alpha ap; scal[irr] = r.r */
+HF_API int hf_cg_update_xr(hf_ws* w, long long n, double* x, double* r, const double* p, const double* ap,
+                           double* scal_dev, int irz, int ipap, int irr, void* stream);
+/* p = z + (scal[irzn]/scal[irz]) p */
+HF_API int hf_cg_update_p(long long n, double* p, const double* z, const double* scal_dev, int irzn, int irz,
+                          void* stream);
+/* z = inv_d r; out_dev[0] = r . z */
+HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, const double* inv_d, double* out_dev,
+                         void* stream);
+/* y = a x + b y */
+HF_API int hf_axpby(long long n, double a, const double* x, double b, double* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HF_H */

@@ -1,0 +1,676 @@
+// C-ABI of the hyperfree-B200 library (libhf.so).  See include/hf.h for the
+// contract and the reference interface each entry point replaces.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hf.h"
+#include "hf_dispatch.h"
+#include "hf_vec.cuh"
+
+using namespace hf;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define HF_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess) return fail(HF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline unsigned vec_blocks(long long n) {
+  long long b = (n + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return (unsigned)b;
+}
+
+// Gauss-Jordan inverse of a small dense matrix (row-major), returns false if singular
+bool invert(std::vector<double> a, int n, std::vector<double>& inv) {
+  inv.assign(n * n, 0.0);
+  for (int i = 0; i < n; ++i) inv[i * n + i] = 1.0;
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(a[r * n + c]) > std::fabs(a[piv * n + c])) piv = r;
+    if (a[piv * n + c] == 0.0) return false;
+    for (int k = 0; k < n; ++k) {
+      std::swap(a[c * n + k], a[piv * n + k]);
+      std::swap(inv[c * n + k], inv[piv * n + k]);
+    }
+    double d = a[c * n + c];
+    for (int k = 0; k < n; ++k) {
+      a[c * n + k] /= d;
+      inv[c * n + k] /= d;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      double f = a[r * n + c];
+      if (f == 0.0) continue;
+      for (int k = 0; k < n; ++k) {
+        a[r * n + k] -= f * a[c * n + k];
+        inv[r * n + k] -= f * inv[c * n + k];
+      }
+    }
+  }
+  return true;
+}
+}  // namespace
+
+struct hf_space {
+  int dim, degree, n1;
+  HfTables tab;
+  HfLattice lat;
+  long long n_dofs;
+  double* d_jinv = nullptr;
+  double* d_jxw = nullptr;
+  double* d_mu = nullptr;
+  double* d_lam = nullptr;
+  uint8_t* d_mask = nullptr;
+  unsigned long long* d_u64 = nullptr;  // [0] detmin [1] detmax [2] first-index
+};
+
+struct hf_tangent {
+  hf_space* sp;
+  int strategy;
+  int nf;
+  double* d_cache = nullptr;
+  double* d_ubar = nullptr;
+};
+
+struct hf_transfer {
+  const hf_space* coarse;
+  const hf_space* fine;
+  // per axis CSR of prolongation (rows: fine) and restriction (rows: coarse)
+  int* d_pp[3] = {nullptr, nullptr, nullptr};
+  int* d_pc[3] = {nullptr, nullptr, nullptr};
+  double* d_pw[3] = {nullptr, nullptr, nullptr};
+  int* d_rp[3] = {nullptr, nullptr, nullptr};
+  int* d_rc[3] = {nullptr, nullptr, nullptr};
+  double* d_rw[3] = {nullptr, nullptr, nullptr};
+  double* d_tmp[2] = {nullptr, nullptr};
+  long long tmp_len = 0;
+};
+
+struct hf_ws {
+  double* d_partials = nullptr;
+  unsigned* d_counter = nullptr;
+};
+
+extern "C" {
+
+HF_API const char* hf_last_error(void) { return g_err.c_str(); }
+HF_API int hf_abi_version(void) { return HF_ABI_VERSION; }
+
+HF_API int hf_max_degree(int dim) { return dim == 2 ? 8 : (dim == 3 ? 4 : 0); }
+
+// ---------------------------------------------------------------------------
+HF_API int hf_space_create(int dim, int degree, int nq1, const int* cells, const double* values_1d,
+                           const double* derivs_1d, const double* qpoints_1d, const double* qweights_1d,
+                           const double* vertices, const double* mu_el, const double* lam_el,
+                           const unsigned char* mask, void* stream, hf_space** out) {
+  if (!out || !cells || !values_1d || !derivs_1d || !qpoints_1d || !qweights_1d || !vertices || !mu_el || !lam_el ||
+      !mask)
+    return fail(HF_ERR_ARG, "hf_space_create: null argument");
+  if (dim != 2 && dim != 3) return fail(HF_ERR_ARG, "dim must be 2 or 3");
+  if (degree < 1 || degree > hf_max_degree(dim))
+    return fail(HF_ERR_UNSUPPORTED, "degree " + std::to_string(degree) + " not instantiated for dim " + std::to_string(dim));
+  if (nq1 != degree + 1)
+    return fail(HF_ERR_UNSUPPORTED, "the B200 kernels are instantiated for n_qpoints = degree + 1 only");
+  hf_space* sp = new hf_space();
+  sp->dim = dim;
+  sp->degree = degree;
+  sp->n1 = degree + 1;
+  const int N = sp->n1;
+  std::memset(&sp->tab, 0, sizeof(HfTables));
+  std::vector<double> V(N * N), Vinv;
+  for (int i = 0; i < N * N; ++i) {
+    sp->tab.V[i] = values_1d[i];
+    sp->tab.D[i] = derivs_1d[i];
+    V[i] = values_1d[i];
+  }
+  for (int i = 0; i < N; ++i) {
+    sp->tab.qp[i] = qpoints_1d[i];
+    sp->tab.qw[i] = qweights_1d[i];
+  }
+  if (!invert(V, N, Vinv)) {
+    delete sp;
+    return fail(HF_ERR_ARG, "singular 1D value table");
+  }
+  // Dco(o, l) = sum_i D[i][o] Vinv[l][i]
+  for (int o = 0; o < N; ++o)
+    for (int l = 0; l < N; ++l) {
+      double s = 0.0;
+      for (int i = 0; i < N; ++i) s += derivs_1d[i * N + o] * Vinv[l * N + i];
+      sp->tab.Dc[l * N + o] = s;   // Dc[l][o]  = Dco(o, l)
+      sp->tab.DcT[o * N + l] = s;  // DcT[o][l] = Dco(o, l)
+    }
+  sp->lat.cells[2] = 1;
+  sp->lat.nodes[2] = 1;
+  long long nel = 1, nn = 1;
+  for (int a = 0; a < dim; ++a) {
+    if (cells[a] < 1) {
+      delete sp;
+      return fail(HF_ERR_ARG, "cells per axis must be >= 1");
+    }
+    sp->lat.cells[a] = cells[a];
+    sp->lat.nodes[a] = cells[a] * degree + 1;
+    nel *= cells[a];
+    nn *= sp->lat.nodes[a];
+  }
+  long long nq = 1;
+  for (int a = 0; a < dim; ++a) nq *= N;
+  sp->lat.n_el = nel;
+  sp->lat.n_nodes = nn;
+  sp->lat.n_qp = nel * nq;
+  sp->n_dofs = nn * dim;
+  cudaStream_t s = S(stream);
+  long long nverts = 1;
+  for (int a = 0; a < dim; ++a) nverts *= (cells[a] + 1);
+  double* d_verts = nullptr;
+#define ALLOC(ptr, bytes) HF_CUDA(cudaMalloc((void**)&(ptr), (bytes)))
+  ALLOC(sp->d_jinv, sizeof(double) * dim * dim * sp->lat.n_qp);
+  ALLOC(sp->d_jxw, sizeof(double) * sp->lat.n_qp);
+  ALLOC(sp->d_mu, sizeof(double) * nel);
+  ALLOC(sp->d_lam, sizeof(double) * nel);
+  ALLOC(sp->d_mask, sp->n_dofs);
+  ALLOC(sp->d_u64, sizeof(unsigned long long) * 4);
+  ALLOC(d_verts, sizeof(double) * nverts * dim);
+  HF_CUDA(cudaMemcpyAsync(d_verts, vertices, sizeof(double) * nverts * dim, cudaMemcpyHostToDevice, s));
+  HF_CUDA(cudaMemcpyAsync(sp->d_mu, mu_el, sizeof(double) * nel, cudaMemcpyHostToDevice, s));
+  HF_CUDA(cudaMemcpyAsync(sp->d_lam, lam_el, sizeof(double) * nel, cudaMemcpyHostToDevice, s));
+  HF_CUDA(cudaMemcpyAsync(sp->d_mask, mask, sp->n_dofs, cudaMemcpyHostToDevice, s));
+  unsigned long long init = ~0ull;
+  HF_CUDA(cudaMemcpyAsync(sp->d_u64, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  HF_CUDA(launch_geometry(dim, sp->tab, sp->lat, N, d_verts, sp->d_jinv, sp->d_jxw, sp->d_u64, s));
+  unsigned long long o = 0;
+  HF_CUDA(cudaMemcpyAsync(&o, sp->d_u64, sizeof(o), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d_verts);
+  if (nel > 0 && !(hf_unord(o) > 0.0)) {
+    hf_space_destroy(sp);
+    char buf[128];
+    std::snprintf(buf, sizeof(buf), "non-positive mapping Jacobian (det=%.3e)", hf_unord(o));
+    return fail(HF_ERR_GEOMETRY, buf);
+  }
+  *out = sp;
+  return HF_OK;
+}
+
+HF_API int hf_space_set_mask(hf_space* sp, const unsigned char* mask, void* stream) {
+  if (!sp || !mask) return fail(HF_ERR_ARG, "null argument");
+  HF_CUDA(cudaMemcpyAsync(sp->d_mask, mask, sp->n_dofs, cudaMemcpyHostToDevice, S(stream)));
+  HF_CUDA(cudaStreamSynchronize(S(stream)));
+  return HF_OK;
+}
+
+HF_API int hf_space_info(const hf_space* sp, long long* n_dofs, long long* n_el, long long* n_qp) {
+  if (!sp) return fail(HF_ERR_ARG, "null space");
+  if (n_dofs) *n_dofs = sp->n_dofs;
+  if (n_el) *n_el = sp->lat.n_el;
+  if (n_qp) *n_qp = sp->lat.n_qp;
+  return HF_OK;
+}
+
+HF_API int hf_space_pointers(const hf_space* sp, const double** jinv, const double** jxw,
+                             const unsigned char** mask) {
+  if (!sp) return fail(HF_ERR_ARG, "null space");
+  if (jinv) *jinv = sp->d_jinv;
+  if (jxw) *jxw = sp->d_jxw;
+  if (mask) *mask = sp->d_mask;
+  return HF_OK;
+}
+
+HF_API int hf_space_geometry_copy(const hf_space* sp, double* jinv_dev, double* jxw_dev, void* stream) {
+  if (!sp || !jinv_dev || !jxw_dev) return fail(HF_ERR_ARG, "null argument");
+  cudaStream_t s = S(stream);
+  HF_CUDA(cudaMemcpyAsync(jinv_dev, sp->d_jinv, sizeof(double) * sp->dim * sp->dim * sp->lat.n_qp,
+                          cudaMemcpyDeviceToDevice, s));
+  HF_CUDA(cudaMemcpyAsync(jxw_dev, sp->d_jxw, sizeof(double) * sp->lat.n_qp, cudaMemcpyDeviceToDevice, s));
+  return HF_OK;
+}
+
+HF_API int hf_space_destroy(hf_space* sp) {
+  if (!sp) return HF_OK;
+  cudaFree(sp->d_jinv);
+  cudaFree(sp->d_jxw);
+  cudaFree(sp->d_mu);
+  cudaFree(sp->d_lam);
+  cudaFree(sp->d_mask);
+  cudaFree(sp->d_u64);
+  delete sp;
+  return HF_OK;
+}
+
+// ---------------------------------------------------------------------------
+static CellArgs base_args(const hf_space* sp) {
+  CellArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.tab = sp->tab;
+  a.lat = sp->lat;
+  a.degree = sp->degree;
+  a.jinv = sp->d_jinv;
+  a.jxw = sp->d_jxw;
+  a.mu = sp->d_mu;
+  a.lam = sp->d_lam;
+  a.mask = sp->d_mask;
+  return a;
+}
+
+static cudaError_t cell(const hf_space* sp, int op, int var, const CellArgs& a, cudaStream_t s, int mode = 0,
+                        double target = 0.0, unsigned long long* first = nullptr) {
+  if (sp->dim == 2) return launch_cell_2d(op, sp->n1, var, a, mode, target, first, s);
+  return launch_cell_3d(op, sp->n1, var, a, mode, target, first, s);
+}
+
+static int nfields(int dim, int strategy) {
+  int nv = dim * (dim + 1) / 2, nm = nv * (nv + 1) / 2;
+  if (strategy == HF_TENSOR4) return nv + nm + dim * dim + 1;
+  if (strategy == HF_TENSOR2) return 2 + nv + dim * dim + 1;
+  return 1;
+}
+
+// locate the first q-point (flat e*nq+q) attaining min det F of state u
+static int locate_min_det(hf_space* sp, const double* u, cudaStream_t s, hf_error_info* err) {
+  CellArgs a = base_args(sp);
+  a.x = u;
+  a.detmin = sp->d_u64;
+  a.detmax = sp->d_u64 + 1;
+  unsigned long long init[3] = {~0ull, 0ull, ~0ull};
+  HF_CUDA(cudaMemcpyAsync(sp->d_u64, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  HF_CUDA(cell(sp, OP_JRANGE, 0, a, s, 0));
+  unsigned long long mm[2];
+  HF_CUDA(cudaMemcpyAsync(mm, sp->d_u64, sizeof(mm), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  double jmin = hf_unord(mm[0]);
+  HF_CUDA(cell(sp, OP_JRANGE, 0, a, s, 1, jmin, sp->d_u64 + 2));
+  unsigned long long idx;
+  HF_CUDA(cudaMemcpyAsync(&idx, sp->d_u64 + 2, sizeof(idx), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  long long nq = sp->lat.n_qp / (sp->lat.n_el > 0 ? sp->lat.n_el : 1);
+  if (err) {
+    err->code = HF_ERR_JACOBIAN;
+    err->det = jmin;
+    err->element = (long long)(idx / (unsigned long long)nq);
+    err->qpoint = (int)(idx % (unsigned long long)nq);
+  }
+  char buf[160];
+  std::snprintf(buf, sizeof(buf), "det F = %.3e <= 0 in element %lld (quadrature point %d)", jmin,
+                (long long)(idx / (unsigned long long)nq), (int)(idx % (unsigned long long)nq));
+  return fail(HF_ERR_JACOBIAN, buf);
+}
+
+HF_API int hf_jacobian_range(hf_space* sp, const double* u_dev, void* stream, double* jmin, double* jmax,
+                             long long* argmin_element, int* argmin_qpoint) {
+  if (!sp || !u_dev) return fail(HF_ERR_ARG, "null argument");
+  cudaStream_t s = S(stream);
+  hf_error_info e;
+  int rc = locate_min_det(sp, u_dev, s, &e);
+  if (rc != HF_ERR_JACOBIAN) return rc;
+  unsigned long long mm[2];
+  HF_CUDA(cudaMemcpyAsync(mm, sp->d_u64, sizeof(mm), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  if (jmin) *jmin = hf_unord(mm[0]);
+  if (jmax) *jmax = hf_unord(mm[1]);
+  if (argmin_element) *argmin_element = e.element;
+  if (argmin_qpoint) *argmin_qpoint = e.qpoint;
+  g_err.clear();
+  return HF_OK;
+}
+
+HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev, void* stream, hf_tangent** out,
+                             hf_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!sp || !ubar_dev || !out) return fail(HF_ERR_ARG, "null argument");
+  if (strategy < HF_SCALAR || strategy > HF_TENSOR4) return fail(HF_ERR_ARG, "unknown strategy");
+  cudaStream_t s = S(stream);
+  hf_tangent* op = new hf_tangent();
+  op->sp = sp;
+  op->strategy = strategy;
+  op->nf = nfields(sp->dim, strategy);
+  HF_CUDA(cudaMalloc((void**)&op->d_cache, sizeof(double) * op->nf * (sp->lat.n_qp > 0 ? sp->lat.n_qp : 1)));
+  if (strategy == HF_SCALAR) {
+    HF_CUDA(cudaMalloc((void**)&op->d_ubar, sizeof(double) * sp->n_dofs));
+    HF_CUDA(cudaMemcpyAsync(op->d_ubar, ubar_dev, sizeof(double) * sp->n_dofs, cudaMemcpyDeviceToDevice, s));
+  }
+  unsigned long long init = ~0ull;
+  HF_CUDA(cudaMemcpyAsync(sp->d_u64, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  CellArgs a = base_args(sp);
+  a.x = ubar_dev;
+  a.cache_out = op->d_cache;
+  a.detmin = sp->d_u64;
+  HF_CUDA(cell(sp, OP_BUILD, strategy, a, s));
+  unsigned long long o;
+  HF_CUDA(cudaMemcpyAsync(&o, sp->d_u64, sizeof(o), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  if (sp->lat.n_el > 0 && !(hf_unord(o) > 0.0)) {
+    hf_tangent_destroy(op);
+    return locate_min_det(sp, ubar_dev, s, err);
+  }
+  *out = op;
+  return HF_OK;
+}
+
+HF_API int hf_tangent_apply_raw(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                void* stream) {
+  if (!op || !x_dev || !y_dev) return fail(HF_ERR_ARG, "null argument");
+  CellArgs a = base_args(op->sp);
+  a.x = x_dev;
+  a.y = y_dev;
+  a.cache = op->d_cache;
+  a.ubar = op->d_ubar;
+  a.skip = skip_dev;
+  HF_CUDA(cell(op->sp, OP_APPLY, op->strategy, a, S(stream)));
+  return HF_OK;
+}
+
+HF_API int hf_tangent_apply_flagged(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                    void* stream) {
+  if (!op || !x_dev || !y_dev) return fail(HF_ERR_ARG, "null argument");
+  const hf_space* sp = op->sp;
+  cudaStream_t s = S(stream);
+  k_fill_masked<<<vec_blocks(sp->n_dofs), 256, 0, s>>>(sp->n_dofs, y_dev, x_dev, sp->d_mask, 0.0, skip_dev);
+  HF_CUDA(cudaGetLastError());
+  return hf_tangent_apply_raw(op, x_dev, y_dev, skip_dev, stream);
+}
+
+HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream) {
+  return hf_tangent_apply_flagged(op, x_dev, y_dev, nullptr, stream);
+}
+
+HF_API int hf_tangent_diagonal(hf_tangent* op, double* d_dev, void* stream) {
+  if (!op || !d_dev) return fail(HF_ERR_ARG, "null argument");
+  const hf_space* sp = op->sp;
+  cudaStream_t s = S(stream);
+  k_fill_masked<<<vec_blocks(sp->n_dofs), 256, 0, s>>>(sp->n_dofs, d_dev, nullptr, sp->d_mask, 1.0, nullptr);
+  HF_CUDA(cudaGetLastError());
+  CellArgs a = base_args(sp);
+  a.y = d_dev;
+  a.cache = op->d_cache;
+  a.ubar = op->d_ubar;
+  HF_CUDA(cell(sp, OP_DIAG, op->strategy, a, s));
+  return HF_OK;
+}
+
+HF_API int hf_tangent_storage(const hf_tangent* op, long long* storage_bytes, int* payload_scalars,
+                              long long* payload_bytes) {
+  if (!op) return fail(HF_ERR_ARG, "null tangent");
+  const hf_space* sp = op->sp;
+  int d = sp->dim, nv = d * (d + 1) / 2;
+  int payload = op->strategy == HF_SCALAR ? 1 : (op->strategy == HF_TENSOR2 ? 2 + nv : nv + nv * (nv + 1) / 2);
+  long long nqp = sp->lat.n_qp;
+  if (payload_scalars) *payload_scalars = payload;
+  if (payload_bytes) *payload_bytes = 8ll * payload * nqp;
+  // operators.py:412-417: payload + (jac_inv or jac_spatial_inv) + jxw
+  if (storage_bytes) *storage_bytes = 8ll * nqp * (payload + d * d + 1);
+  return HF_OK;
+}
+
+HF_API int hf_tangent_destroy(hf_tangent* op) {
+  if (!op) return HF_OK;
+  cudaFree(op->d_cache);
+  cudaFree(op->d_ubar);
+  delete op;
+  return HF_OK;
+}
+
+// ---------------------------------------------------------------------------
+HF_API int hf_residual(hf_space* sp, const double* u_dev, const double* traction, const double* surf_w_dev,
+                       double* out_dev, void* stream, hf_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!sp || !u_dev || !out_dev) return fail(HF_ERR_ARG, "null argument");
+  if (traction && !surf_w_dev) return fail(HF_ERR_ARG, "traction needs surface weights");
+  cudaStream_t s = S(stream);
+  HF_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * sp->n_dofs, s));
+  unsigned long long init = ~0ull;
+  HF_CUDA(cudaMemcpyAsync(sp->d_u64, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  CellArgs a = base_args(sp);
+  a.x = u_dev;
+  a.y = out_dev;
+  a.detmin = sp->d_u64;
+  HF_CUDA(cell(sp, OP_RESIDUAL, 0, a, s));
+  double t[3] = {0, 0, 0};
+  if (traction)
+    for (int i = 0; i < sp->dim; ++i) t[i] = traction[i];
+  k_resid_finalize<<<vec_blocks(sp->n_dofs), 256, 0, s>>>(sp->lat.n_nodes, sp->dim, out_dev, surf_w_dev, t[0], t[1],
+                                                          t[2], traction ? 1 : 0, sp->d_mask);
+  HF_CUDA(cudaGetLastError());
+  unsigned long long o;
+  HF_CUDA(cudaMemcpyAsync(&o, sp->d_u64, sizeof(o), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  if (sp->lat.n_el > 0 && !(hf_unord(o) > 0.0)) return locate_min_det(sp, u_dev, s, err);
+  return HF_OK;
+}
+
+// ---------------------------------------------------------------------------
+HF_API int hf_transfer_create(const hf_space* coarse, const hf_space* fine, const double* const* interp_1d,
+                              hf_transfer** out) {
+  if (!coarse || !fine || !interp_1d || !out) return fail(HF_ERR_ARG, "null argument");
+  if (coarse->dim != fine->dim || coarse->degree != fine->degree) return fail(HF_ERR_ARG, "incompatible levels");
+  for (int a = 0; a < coarse->dim; ++a)
+    if (fine->lat.cells[a] != 2 * coarse->lat.cells[a])
+      return fail(HF_ERR_ARG, "transfer requires a 2:1 refined pair of levels");
+  hf_transfer* t = new hf_transfer();
+  t->coarse = coarse;
+  t->fine = fine;
+  for (int a = 0; a < coarse->dim; ++a) {
+    int nf = fine->lat.nodes[a], nc = coarse->lat.nodes[a];
+    const double* M = interp_1d[a];  // (nf, nc) row-major
+    std::vector<int> pp(1, 0), pc, rp(1, 0), rc;
+    std::vector<double> pw, rw;
+    for (int f = 0; f < nf; ++f) {
+      for (int c = 0; c < nc; ++c)
+        if (M[(long long)f * nc + c] != 0.0) {
+          pc.push_back(c);
+          pw.push_back(M[(long long)f * nc + c]);
+        }
+      pp.push_back((int)pc.size());
+    }
+    for (int c = 0; c < nc; ++c) {
+      for (int f = 0; f < nf; ++f)
+        if (M[(long long)f * nc + c] != 0.0) {
+          rc.push_back(f);
+          rw.push_back(M[(long long)f * nc + c]);
+        }
+      rp.push_back((int)rc.size());
+    }
+    HF_CUDA(cudaMalloc((void**)&t->d_pp[a], sizeof(int) * pp.size()));
+    HF_CUDA(cudaMalloc((void**)&t->d_pc[a], sizeof(int) * (pc.size() + 1)));
+    HF_CUDA(cudaMalloc((void**)&t->d_pw[a], sizeof(double) * (pw.size() + 1)));
+    HF_CUDA(cudaMalloc((void**)&t->d_rp[a], sizeof(int) * rp.size()));
+    HF_CUDA(cudaMalloc((void**)&t->d_rc[a], sizeof(int) * (rc.size() + 1)));
+    HF_CUDA(cudaMalloc((void**)&t->d_rw[a], sizeof(double) * (rw.size() + 1)));
+    HF_CUDA(cudaMemcpy(t->d_pp[a], pp.data(), sizeof(int) * pp.size(), cudaMemcpyHostToDevice));
+    HF_CUDA(cudaMemcpy(t->d_pc[a], pc.data(), sizeof(int) * pc.size(), cudaMemcpyHostToDevice));
+    HF_CUDA(cudaMemcpy(t->d_pw[a], pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice));
+    HF_CUDA(cudaMemcpy(t->d_rp[a], rp.data(), sizeof(int) * rp.size(), cudaMemcpyHostToDevice));
+    HF_CUDA(cudaMemcpy(t->d_rc[a], rc.data(), sizeof(int) * rc.size(), cudaMemcpyHostToDevice));
+    HF_CUDA(cudaMemcpy(t->d_rw[a], rw.data(), sizeof(double) * rw.size(), cudaMemcpyHostToDevice));
+  }
+  // largest intermediate: fine nodes (all passes are bounded by the fine lattice)
+  t->tmp_len = fine->n_dofs;
+  HF_CUDA(cudaMalloc((void**)&t->d_tmp[0], sizeof(double) * t->tmp_len));
+  HF_CUDA(cudaMalloc((void**)&t->d_tmp[1], sizeof(double) * t->tmp_len));
+  *out = t;
+  return HF_OK;
+}
+
+// mode: 0 plain, 1 zero constrained outputs, 2 add into out with constrained dropped
+static int transfer_run(hf_transfer* t, bool prolong, const double* in, double* out, int mode, cudaStream_t s) {
+  const hf_space* src = prolong ? t->coarse : t->fine;
+  const hf_space* dst = prolong ? t->fine : t->coarse;
+  int dim = src->dim, C = dim;
+  int n[3] = {src->lat.nodes[0], src->lat.nodes[1], dim == 3 ? src->lat.nodes[2] : 1};
+  const double* cur = in;
+  for (int a = 0; a < dim; ++a) {
+    bool last = (a == dim - 1);
+    double* dst_buf = last ? out : t->d_tmp[a & 1];
+    int nout = dst->lat.nodes[a];
+    long long total = (long long)C * nout * (a == 0 ? 1 : n[0]) * (a == 1 ? 1 : n[1]) * (a == 2 ? 1 : n[2]);
+    if (a == 0) total = (long long)C * nout * n[1] * n[2];
+    else if (a == 1) total = (long long)C * n[0] * nout * n[2];
+    else total = (long long)C * n[0] * n[1] * nout;
+    k_axis<<<vec_blocks(total), 256, 0, s>>>(cur, dst_buf, n[0], n[1], n[2], C, a, nout,
+                                             prolong ? t->d_pp[a] : t->d_rp[a], prolong ? t->d_pc[a] : t->d_rc[a],
+                                             prolong ? t->d_pw[a] : t->d_rw[a], dst->d_mask, last ? mode : 0);
+    HF_CUDA(cudaGetLastError());
+    n[a] = nout;
+    cur = dst_buf;
+  }
+  return HF_OK;
+}
+
+HF_API int hf_prolong(hf_transfer* t, const double* xc, double* xf, int mode, void* stream) {
+  if (!t || !xc || !xf) return fail(HF_ERR_ARG, "null argument");
+  return transfer_run(t, true, xc, xf, mode, S(stream));
+}
+
+HF_API int hf_restrict(hf_transfer* t, const double* rf, double* rc, int mode, void* stream) {
+  if (!t || !rf || !rc) return fail(HF_ERR_ARG, "null argument");
+  return transfer_run(t, false, rf, rc, mode, S(stream));
+}
+
+HF_API int hf_transfer_destroy(hf_transfer* t) {
+  if (!t) return HF_OK;
+  for (int a = 0; a < 3; ++a) {
+    cudaFree(t->d_pp[a]);
+    cudaFree(t->d_pc[a]);
+    cudaFree(t->d_pw[a]);
+    cudaFree(t->d_rp[a]);
+    cudaFree(t->d_rc[a]);
+    cudaFree(t->d_rw[a]);
+  }
+  cudaFree(t->d_tmp[0]);
+  cudaFree(t->d_tmp[1]);
+  delete t;
+  return HF_OK;
+}
+
+HF_API int hf_inject(const hf_space* coarse, const hf_space* fine, const double* uf, double* uc, int keep_constrained,
+                     void* stream) {
+  if (!coarse || !fine || !uf || !uc) return fail(HF_ERR_ARG, "null argument");
+  for (int a = 0; a < coarse->dim; ++a)
+    if (fine->lat.nodes[a] != 2 * coarse->lat.nodes[a] - 1) return fail(HF_ERR_ARG, "levels are not 2:1 nested");
+  k_inject<<<vec_blocks(coarse->n_dofs), 256, 0, S(stream)>>>(uf, uc, coarse->lat.nodes[0], coarse->lat.nodes[1],
+                                                              coarse->dim == 3 ? coarse->lat.nodes[2] : 1,
+                                                              fine->lat.nodes[0], fine->lat.nodes[1], coarse->dim,
+                                                              coarse->d_mask, keep_constrained);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+// ---------------------------------------------------------------------------
+HF_API int hf_ws_create(hf_ws** out) {
+  if (!out) return fail(HF_ERR_ARG, "null argument");
+  hf_ws* w = new hf_ws();
+  HF_CUDA(cudaMalloc((void**)&w->d_partials, sizeof(double) * RED_MAX_BLOCKS));
+  HF_CUDA(cudaMalloc((void**)&w->d_counter, sizeof(unsigned)));
+  HF_CUDA(cudaMemset(w->d_counter, 0, sizeof(unsigned)));
+  *out = w;
+  return HF_OK;
+}
+
+HF_API int hf_ws_destroy(hf_ws* w) {
+  if (!w) return HF_OK;
+  cudaFree(w->d_partials);
+  cudaFree(w->d_counter);
+  delete w;
+  return HF_OK;
+}
+
+HF_API int hf_dot(hf_ws* w, long long n, const double* a, const double* b, double* out_dev, const int* skip_dev,
+                  void* stream) {
+  if (!w || !a || !b || !out_dev) return fail(HF_ERR_ARG, "null argument");
+  k_dot<<<red_blocks(n), RED_THREADS, 0, S(stream)>>>(n, a, b, w->d_partials, w->d_counter, out_dev, skip_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_fill_masked(long long n, double* y, const double* x, const unsigned char* mask, double masked_value,
+                          void* stream) {
+  if (!y || !mask) return fail(HF_ERR_ARG, "null argument");
+  k_fill_masked<<<vec_blocks(n), 256, 0, S(stream)>>>(n, y, x, mask, masked_value, nullptr);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_cheb_step(long long n, double* x, double* d, const double* b, const double* ax, const double* inv_d,
+                        int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
+                        void* stream) {
+  if (!x || !d || !b || !inv_d) return fail(HF_ERR_ARG, "null argument");
+  k_cheb<<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_resid_masked(long long n, double* r, const double* b, const double* ax, const unsigned char* mask,
+                           void* stream) {
+  if (!r || !b || !ax || !mask) return fail(HF_ERR_ARG, "null argument");
+  k_resid_masked<<<vec_blocks(n), 256, 0, S(stream)>>>(n, r, b, ax, mask);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_resnorm_check(hf_ws* w, long long n, const double* b, const double* ax, double* scal, int out_idx,
+                            int target_idx, int* flag_dev, void* stream) {
+  if (!w || !b || !ax || !scal || !flag_dev) return fail(HF_ERR_ARG, "null argument");
+  cudaStream_t s = S(stream);
+  k_resnorm_check<<<red_blocks(n), RED_THREADS, 0, s>>>(n, b, ax, w->d_partials, w->d_counter, scal, out_idx,
+                                                         target_idx, flag_dev);
+  k_scalar<<<1, 32, 0, s>>>(0, scal, out_idx, target_idx, 0.0, flag_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_scalar_op(int op, double* scal, int a, int b, double rel, int* flag_dev, void* stream) {
+  if (!scal || !flag_dev) return fail(HF_ERR_ARG, "null argument");
+  k_scalar<<<1, 32, 0, S(stream)>>>(op, scal, a, b, rel, flag_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_cg_update_xr(hf_ws* w, long long n, double* x, double* r, const double* p, const double* ap,
+                           double* scal, int irz, int ipap, int irr, void* stream) {
+  if (!w || !x || !r || !p || !ap || !scal) return fail(HF_ERR_ARG, "null argument");
+  k_cg_xr<<<red_blocks(n), RED_THREADS, 0, S(stream)>>>(n, x, r, p, ap, scal, irz, ipap, irr, w->d_partials,
+                                                       w->d_counter);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_cg_update_p(long long n, double* p, const double* z, const double* scal, int irzn, int irz,
+                          void* stream) {
+  if (!p || !z || !scal) return fail(HF_ERR_ARG, "null argument");
+  k_cg_p<<<vec_blocks(n), 256, 0, S(stream)>>>(n, p, z, scal, irzn, irz);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, const double* inv_d, double* out_dev,
+                         void* stream) {
+  if (!w || !z || !r || !inv_d || !out_dev) return fail(HF_ERR_ARG, "null argument");
+  k_jacobi_dot<<<red_blocks(n), RED_THREADS, 0, S(stream)>>>(n, z, r, inv_d, w->d_partials, w->d_counter, out_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_axpby(long long n, double a, const double* x, double b, double* y, void* stream) {
+  if (!x || !y) return fail(HF_ERR_ARG, "null argument");
+  k_axpby<<<vec_blocks(n), 256, 0, S(stream)>>>(n, a, x, b, y);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// Shared device helpers for the hyperfree-B200 kernels (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define HF_DEV __device__ __forceinline__
+
+// Largest 1D table the cell kernels are instantiated for (2D p<=8).
+#define HF_MAXN 9
+
+// 1D data of one level, passed by value as a kernel parameter (lives in the
+// constant bank) and copied to shared memory at kernel start.
+//   V[l*N+o]   = N_l(xi_o)           value of node-basis l at Gauss point o
+//   D[l*N+o]   = N_l'(xi_o)
+//   Dc[l*N+o]  = Dco(o,l)            collocation derivative at point o of the
+//                                    Gauss-point Lagrange basis l  (Dco = D^T V^-T)
+//   DcT[l*N+o] = Dco(l,o)
+//   qp[o], qw[o]                     Gauss points / weights on [0,1]
+struct HfTables {
+  double V[HF_MAXN * HF_MAXN];
+  double D[HF_MAXN * HF_MAXN];
+  double Dc[HF_MAXN * HF_MAXN];
+  double DcT[HF_MAXN * HF_MAXN];
+  double qp[HF_MAXN];
+  double qw[HF_MAXN];
+};
+
+// Per-level geometry/lattice description shared by every cell kernel.
+struct HfLattice {
+  int cells[3];   // cells per axis (x, y, z)
+  int nodes[3];   // lattice nodes per axis (cells*p+1)
+  long long n_el;
+  long long n_nodes;
+  long long n_qp;  // n_el * nq
+};
+
+// ---- ordered-double atomics (min/max of doubles through uint64 atomics) ----
+HF_DEV unsigned long long hf_ord(double v) {
+  unsigned long long b = __double_as_longlong(v);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+static inline __host__ __device__ double hf_unord(unsigned long long o) {
+  unsigned long long b = (o & 0x8000000000000000ull) ? (o & 0x7fffffffffffffffull) : ~o;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)b);
+#else
+  union { unsigned long long u; double d; } cv;
+  cv.u = b;
+  return cv.d;
+#endif
+}
+HF_DEV void hf_atomic_min_d(unsigned long long* a, double v) { atomicMin(a, hf_ord(v)); }
+HF_DEV void hf_atomic_max_d(unsigned long long* a, double v) { atomicMax(a, hf_ord(v)); }
+
+// 3x3 / 2x2 helpers on row-major arrays
+template <int D>
+HF_DEV double hf_det(const double* a);
+template <>
+HF_DEV double hf_det<2>(const double* a) { return a[0] * a[3] - a[1] * a[2]; }
+template <>
+HF_DEV double hf_det<3>(const double* a) {
+  return a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) +
+         a[2] * (a[3] * a[7] - a[4] * a[6]);
+}
+// inverse via adjugate / det
+template <int D>
+HF_DEV void hf_inv(const double* a, double det, double* o);
+template <>
+HF_DEV void hf_inv<2>(const double* a, double det, double* o) {
+  double r = 1.0 / det;
+  o[0] = a[3] * r; o[1] = -a[1] * r; o[2] = -a[2] * r; o[3] = a[0] * r;
+}
+template <>
+HF_DEV void hf_inv<3>(const double* a, double det, double* o) {
+  double r = 1.0 / det;
+  o[0] = (a[4] * a[8] - a[5] * a[7]) * r;
+  o[1] = (a[2] * a[7] - a[1] * a[8]) * r;
+  o[2] = (a[1] * a[5] - a[2] * a[4]) * r;
+  o[3] = (a[5] * a[6] - a[3] * a[8]) * r;
+  o[4] = (a[0] * a[8] - a[2] * a[6]) * r;
+  o[5] = (a[2] * a[3] - a[0] * a[5]) * r;
+  o[6] = (a[3] * a[7] - a[4] * a[6]) * r;
+  o[7] = (a[1] * a[6] - a[0] * a[7]) * r;
+  o[8] = (a[0] * a[4] - a[1] * a[3]) * r;
+}
+
+// Symmetric packing order of the reference (material.py:161-164)
+//   2D: (00, 11, 01)       3D: (00, 11, 22, 12, 02, 01)
+template <int D> struct HfSym;
+template <> struct HfSym<2> {
+  static constexpr int NV = 3;
+  HF_DEV static int a(int k) { return k == 2 ? 0 : k; }
+  HF_DEV static int b(int k) { return k == 2 ? 1 : k; }
+};
+template <> struct HfSym<3> {
+  static constexpr int NV = 6;
+  HF_DEV static int a(int k) { return k < 3 ? k : (k == 3 ? 1 : 0); }
+  HF_DEV static int b(int k) { return k < 3 ? k : (k == 5 ? 1 : 2); }
+};
+// index of the symmetric slot holding (i, j)
+//   3D: (1,2)->3, (0,2)->4, (0,1)->5
+template <int D>
+HF_DEV constexpr int hf_slot(int i, int j) {
+  return (i == j) ? i : (D == 2 ? 2 : (i + j == 3 ? 3 : (i + j == 2 ? 4 : 5)));
+}
+
+// packed upper-triangle (row-major) index of Voigt entry (r, c), r <= c
+template <int NV>
+HF_DEV constexpr int hf_triu(int r, int c) {
+  return r * NV - (r * (r - 1)) / 2 + (c - r);
+}

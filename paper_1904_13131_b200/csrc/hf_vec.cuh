@@ -1,0 +1,223 @@
+// Vector, reduction and grid-transfer kernels (fp64, HBM-bound, grid-stride).
+#pragma once
+#include "hf_common.cuh"
+
+namespace hf {
+
+constexpr int RED_THREADS = 256;
+constexpr int RED_MAX_BLOCKS = 592;  // 4 x 148 SMs
+
+HF_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic grid reduction: per-block partial sums, the last block to
+// finish adds them in block order.  `out` receives the total.
+HF_DEV void grid_reduce(double v, double* partials, unsigned* counter, double* out) {
+  __shared__ double sh[RED_THREADS / 32];
+  __shared__ bool last;
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    v = warp_sum(v);
+    if (lane == 0) {
+      partials[blockIdx.x] = v;
+      __threadfence();
+      unsigned t = atomicAdd(counter, 1u);
+      last = (t == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (last) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(partials + i);
+    s = warp_sum(s);
+    if (lane == 0) sh[w] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
+      *out = t;
+      *counter = 0u;
+    }
+  }
+}
+
+inline unsigned red_blocks(long long n) {
+  long long b = (n + RED_THREADS * 4 - 1) / (RED_THREADS * 4);
+  if (b < 1) b = 1;
+  if (b > RED_MAX_BLOCKS) b = RED_MAX_BLOCKS;
+  return (unsigned)b;
+}
+
+__global__ void k_dot(long long n, const double* __restrict__ a, const double* __restrict__ b, double* partials,
+                      unsigned* counter, double* out, const int* skip) {
+  if (skip && *skip) return;
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    s = fma(a[i], b[i], s);
+  grid_reduce(s, partials, counter, out);
+}
+
+// y[i] = mask[i] ? (x ? x[i] : mval) : 0
+__global__ void k_fill_masked(long long n, double* __restrict__ y, const double* __restrict__ x,
+                              const uint8_t* __restrict__ mask, double mval, const int* skip) {
+  if (skip && *skip) return;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = mask[i] ? (x ? x[i] : mval) : 0.0;
+}
+
+// Chebyshev step (multigrid.py:176-205, 280-296):
+//   z = inv_d * (b - ax)        (ax == nullptr -> A x = 0)
+//   first:  d = z / theta       else d = cd * d + cz * z
+//   x = (x_zero ? 0 : x) + d
+__global__ void k_cheb(long long n, double* __restrict__ x, double* __restrict__ d, const double* __restrict__ b,
+                       const double* __restrict__ ax, const double* __restrict__ inv_d, int first, double theta,
+                       double cd, double cz, int x_zero, const int* skip) {
+  if (skip && *skip) return;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double z = inv_d[i] * (b[i] - (ax ? ax[i] : 0.0));
+    double di = first ? z / theta : cd * d[i] + cz * z;
+    d[i] = di;
+    x[i] = x_zero ? di : x[i] + di;
+  }
+}
+
+// r = b - ax, r[mask] = 0
+__global__ void k_resid_masked(long long n, double* __restrict__ r, const double* __restrict__ b,
+                               const double* __restrict__ ax, const uint8_t* __restrict__ mask) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    r[i] = mask[i] ? 0.0 : b[i] - ax[i];
+}
+
+// ||b - ax||^2 -> scal[out]; if sqrt(.) <= scal[tgt] set *flag (coarse_solve check)
+__global__ void k_resnorm_check(long long n, const double* __restrict__ b, const double* __restrict__ ax,
+                                double* partials, unsigned* counter, double* scal, int out, int tgt, int* flag) {
+  if (*flag) return;
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double r = b[i] - ax[i];
+    s = fma(r, r, s);
+  }
+  grid_reduce(s, partials, counter, scal + out);
+  // the last block wrote scal[out]; the flag is set by a follow-up scalar kernel
+}
+
+// scalar bookkeeping kernels (single thread)
+// op 0: flag = sqrt(scal[a]) <= scal[b]
+// op 1: scal[b] = rel * sqrt(scal[a]); flag = (scal[a] == 0)
+__global__ void k_scalar(int op, double* scal, int a, int b, double rel, int* flag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (op == 0) {
+    if (!*flag && sqrt(scal[a]) <= scal[b]) *flag = 1;
+  } else if (op == 1) {
+    scal[b] = rel * sqrt(scal[a]);
+    *flag = (scal[a] == 0.0) ? 1 : 0;
+  }
+}
+
+// CG updates (solver.py:57-75) with device-resident scalars
+//   alpha = scal[irz] / scal[ipap];  x += alpha p;  r -= alpha ap;  scal[irr] = r.r
+__global__ void k_cg_xr(long long n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                        const double* __restrict__ ap, double* scal, int irz, int ipap, int irr, double* partials,
+                        unsigned* counter) {
+  const double alpha = scal[irz] / scal[ipap];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    double ri = r[i] - alpha * ap[i];
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  grid_reduce(s, partials, counter, scal + irr);
+}
+
+//   beta = scal[irzn] / scal[irz];  p = z + beta p
+__global__ void k_cg_p(long long n, double* __restrict__ p, const double* __restrict__ z, const double* scal, int irzn,
+                       int irz) {
+  const double beta = scal[irzn] / scal[irz];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+
+// z = inv_d * r; scal[out] = r.z  (Jacobi-preconditioned Lanczos, multigrid.py:126-153)
+__global__ void k_jacobi_dot(long long n, double* __restrict__ z, const double* __restrict__ r,
+                             const double* __restrict__ inv_d, double* partials, unsigned* counter, double* out) {
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double zi = inv_d[i] * r[i];
+    z[i] = zi;
+    s = fma(r[i], zi, s);
+  }
+  grid_reduce(s, partials, counter, out);
+}
+
+// y = a x + b y  (general axpby)
+__global__ void k_axpby(long long n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * x[i] + (b == 0.0 ? 0.0 : b * y[i]);
+}
+
+// out[node*C + c] -= traction[c] * sw[node]; out[mask] = 0   (operators.py:221-223)
+__global__ void k_resid_finalize(long long n_nodes, int C, double* __restrict__ out, const double* __restrict__ sw,
+                                 double t0, double t1, double t2, int has_traction, const uint8_t* __restrict__ mask) {
+  const double tr[3] = {t0, t1, t2};
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_nodes * C;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = out[i];
+    if (has_traction) v -= tr[i % C] * sw[i / C];
+    out[i] = mask[i] ? 0.0 : v;
+  }
+}
+
+// One axis of a tensor-product 1D operator on a (n2, n1, n0, C) lattice array
+// (multigrid.py:39-55).  Row o of the banded 1D matrix is (cols, w)[rowptr[o]..].
+// mode 0: out = v;  mode 1: out = mask ? 0 : v;  mode 2: out += mask ? 0 : v
+__global__ void k_axis(const double* __restrict__ in, double* __restrict__ out, int n0, int n1, int n2, int C,
+                       int axis, int nout, const int* __restrict__ rowptr, const int* __restrict__ cols,
+                       const double* __restrict__ w, const uint8_t* __restrict__ mask, int mode) {
+  int m0 = axis == 0 ? nout : n0, m1 = axis == 1 ? nout : n1, m2 = axis == 2 ? nout : n2;
+  long long total = (long long)m0 * m1 * m2 * C;
+  long long in_stride = axis == 0 ? C : (axis == 1 ? (long long)n0 * C : (long long)n0 * n1 * C);
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    long long r = t;
+    int c = (int)(r % C);
+    r /= C;
+    int i0 = (int)(r % m0);
+    r /= m0;
+    int i1 = (int)(r % m1);
+    int i2 = (int)(r / m1);
+    int o = axis == 0 ? i0 : (axis == 1 ? i1 : i2);
+    long long base = (((long long)(axis == 2 ? 0 : i2) * n1 + (axis == 1 ? 0 : i1)) * n0 + (axis == 0 ? 0 : i0)) * C + c;
+    double s = 0.0;
+    for (int k = rowptr[o]; k < rowptr[o + 1]; ++k) s = fma(w[k], in[base + (long long)cols[k] * in_stride], s);
+    if (mode == 0) out[t] = s;
+    else if (mode == 1) out[t] = mask[t] ? 0.0 : s;
+    else if (!mask[t]) out[t] += s;
+  }
+}
+
+// nodal injection onto the coarse lattice (multigrid.py:76-92)
+__global__ void k_inject(const double* __restrict__ uf, double* __restrict__ uc, int nc0, int nc1, int nc2, int nf0,
+                         int nf1, int C, const uint8_t* __restrict__ cmask, int keep) {
+  long long total = (long long)nc0 * nc1 * nc2 * C;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    long long r = t;
+    int c = (int)(r % C);
+    r /= C;
+    int i0 = (int)(r % nc0);
+    r /= nc0;
+    int i1 = (int)(r % nc1);
+    int i2 = (int)(r / nc1);
+    long long f = (((long long)(2 * i2) * nf1 + 2 * i1) * nf0 + 2 * i0) * C + c;
+    double v = uf[f];
+    uc[t] = (!keep && cmask[t]) ? 0.0 : v;
+  }
+}
+
+}  // namespace hf

@@ -1,0 +1,412 @@
+"""Geometric multigrid on the B200 (reference multigrid.py:1-382).
+
+Same algorithm and API as the reference: level tangents linearised at the
+nodal injection of the fine state, Kronecker 1D transfers (restriction = the
+transpose), CG/Lanczos eigenvalue range, restarted Chebyshev smoothing of
+degree 4 on [0.6, 1.2] lambda_max, continuous Chebyshev coarse solve to 1e-3
+with a 100-application cap, V-cycle with 2 pre/post steps.
+
+Device design: every vector lives in a per-level preallocated buffer; each
+step is one fused libhf kernel (apply, Chebyshev update, masked residual,
+transfer passes).  The coarse solve's convergence test is evaluated on the
+device (a flag that turns the remaining kernels into no-ops), so one whole
+V-cycle is a fixed launch sequence that ``GMGPreconditioner`` captures once
+into a CUDA graph and replays per application.
+
+Deviation (documented in DESIGN.md): the first operator application of the
+pre-smoother acts on the zero vector and is skipped (A 0 = 0 exactly).
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+import logging
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.linalg
+import torch
+
+from . import device as dv
+from ._lib import check, lib
+from .fespace import interpolation_matrix_1d
+from .material import NonPositiveJacobian
+from .operators import MatrixFreeTangent, Problem
+
+log = logging.getLogger(__name__)
+
+
+def _apply_into(op, x, y, skip=None):
+    if hasattr(op, "apply_into"):
+        return op.apply_into(x, y, skip)
+    y.copy_(op(x))
+    return y
+
+
+class TransferOperator:
+    """Embedding of a coarse tensor-product space into the 2:1 refined one (multigrid.py:27-55)."""
+
+    def __init__(self, coarse: Problem, fine: Problem):
+        if any(f != 2 * c for f, c in zip(fine.mesh.cells, coarse.mesh.cells)):
+            raise ValueError("transfer requires a 2:1 refined pair of levels")
+        self.coarse, self.fine = coarse, fine
+        self.dim = coarse.dim
+        self.components = coarse.dofmap.components
+        self.coarse_nodes_1d = coarse.dofmap.nodes_per_side
+        self.fine_nodes_1d = fine.dofmap.nodes_per_side
+        self.matrices_1d = [np.ascontiguousarray(interpolation_matrix_1d(coarse.degree, m, coarse.basis.nodes))
+                            for m in coarse.mesh.cells]
+        self.matrix_1d = self.matrices_1d[0]
+        ptrs = (ct.c_void_p * 3)(*[m.ctypes.data for m in self.matrices_1d] + [None] * (3 - self.dim))
+        h = ct.c_void_p()
+        check(lib().hf_transfer_create(coarse._space, fine._space, ptrs, ct.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().hf_transfer_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def prolong_into(self, xc, xf, mode: int = 0):
+        check(lib().hf_prolong(self._h, dv.ptr(xc), dv.ptr(xf), mode, dv.stream()))
+        return xf
+
+    def restrict_into(self, rf, rc, mode: int = 0):
+        check(lib().hf_restrict(self._h, dv.ptr(rf), dv.ptr(rc), mode, dv.stream()))
+        return rc
+
+    def prolong(self, x_coarse):
+        xc = dv.as_dev(x_coarse)
+        out = torch.empty(self.fine.n_dofs, dtype=torch.float64, device="cuda")
+        return dv.like_input(self.prolong_into(xc, out), x_coarse)
+
+    def restrict(self, r_fine):
+        rf = dv.as_dev(r_fine)
+        out = torch.empty(self.coarse.n_dofs, dtype=torch.float64, device="cuda")
+        return dv.like_input(self.restrict_into(rf, out), r_fine)
+
+
+def restrict_solution(problems: list[Problem], u_fine, keep_constrained: bool = False):
+    """Nodal injection of the finest displacement onto every level (multigrid.py:76-92).
+
+    ``keep_constrained`` keeps prescribed Dirichlet values on the levels
+    (needed for non-homogeneous constraints); the reference resets
+    them to zero."""
+    levels = [dv.as_dev(u_fine)]
+    for lvl in range(len(problems) - 1, 0, -1):
+        fp, cp = problems[lvl], problems[lvl - 1]
+        uc = torch.empty(cp.n_dofs, dtype=torch.float64, device="cuda")
+        check(lib().hf_inject(cp._space, fp._space, dv.ptr(levels[0]), dv.ptr(uc), int(keep_constrained),
+                              dv.stream()))
+        levels.insert(0, uc)
+    if not isinstance(u_fine, torch.Tensor):
+        return [v.cpu().numpy() for v in levels]
+    return levels
+
+
+_RHS_CACHE: dict = {}
+
+
+def _lanczos_rhs(n: int, seed: int, mask: np.ndarray | None) -> torch.Tensor:
+    """b = default_rng(seed).standard_normal(n), constrained = 0 (multigrid.py:121-124), cached on device."""
+    key = (n, seed, None if mask is None else hash(mask.tobytes()))
+    if key not in _RHS_CACHE:
+        b = np.random.default_rng(seed).standard_normal(n)
+        if mask is not None:
+            b[mask] = 0.0
+        _RHS_CACHE[key] = dv.as_dev(b)
+    return _RHS_CACHE[key]
+
+
+def estimate_eigenvalue_range(apply_fn, diagonal, seed: int = 0, iterations: int = 30,
+                              constrained: np.ndarray | None = None) -> tuple[float, float]:
+    """Smallest and largest Ritz values of D^-1 A from a Jacobi-PCG/Lanczos run
+    (multigrid.py:112-166).  Vector work and dots on the device; the k x k
+    tridiagonal eigenproblem on the host with the reference's scipy call."""
+    diag = dv.as_dev(diagonal)
+    n = diag.numel()
+    b = _lanczos_rhs(n, seed, constrained)
+    inv_d = torch.reciprocal(diag)
+    r = b.clone()
+    z = torch.empty_like(r)
+    ap = torch.empty_like(r)
+    scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+    ws = dv.Workspace.get().handle
+    L = lib()
+    check(L.hf_jacobi_dot(ws, n, dv.ptr(z), dv.ptr(r), dv.ptr(inv_d), dv.ptr(scal[0:1]), dv.stream()))
+    p = z.clone()
+    rz = float(scal[0].item())
+    alphas: list[float] = []
+    betas: list[float] = []
+    for _ in range(iterations):
+        if rz <= 0.0 or not np.isfinite(rz):
+            break
+        _apply_into(apply_fn, p, ap)
+        dv.dot(p, ap, scal[1:2])
+        pap = float(scal[1].item())
+        if pap <= 0.0:
+            break
+        alpha = rz / pap
+        check(L.hf_axpby(n, -alpha, dv.ptr(ap), 1.0, dv.ptr(r), dv.stream()))
+        check(L.hf_jacobi_dot(ws, n, dv.ptr(z), dv.ptr(r), dv.ptr(inv_d), dv.ptr(scal[2:3]), dv.stream()))
+        rz_new = float(scal[2].item())
+        if rz_new <= 1e-28 * rz or not np.isfinite(rz_new):
+            alphas.append(alpha)
+            break
+        beta = rz_new / rz
+        alphas.append(alpha)
+        betas.append(beta)
+        check(L.hf_axpby(n, 1.0, dv.ptr(z), beta, dv.ptr(p), dv.stream()))
+        rz = rz_new
+    if not alphas:
+        return 1.0, 1.0
+    k = len(alphas)
+    diag_t = np.empty(k)
+    diag_t[0] = 1.0 / alphas[0]
+    for i in range(1, k):
+        diag_t[i] = 1.0 / alphas[i] + betas[i - 1] / alphas[i - 1]
+    off_t = np.array([np.sqrt(betas[i]) / alphas[i] for i in range(k - 1)])
+    if k == 1:
+        return float(diag_t[0]), float(diag_t[0])
+    ritz = scipy.linalg.eigvalsh_tridiagonal(diag_t, off_t)
+    return float(ritz[0]), float(ritz[-1])
+
+
+def estimate_lambda_max(apply_fn, diagonal, seed=0, iterations=30, constrained=None) -> float:
+    return estimate_eigenvalue_range(apply_fn, diagonal, seed, iterations, constrained)[1]
+
+
+@dataclass(frozen=True)
+class ChebyshevSettings:
+    degree: int = 4
+    range_lo: float = 0.6
+    range_hi: float = 1.2
+
+
+def _cheb_coeffs(lam_max: float, s: ChebyshevSettings):
+    theta = 0.5 * (s.range_hi + s.range_lo) * lam_max
+    delta = 0.5 * (s.range_hi - s.range_lo) * lam_max
+    sigma = theta / delta
+    coefs = []
+    rho_old = 1.0 / sigma
+    for _ in range(s.degree - 1):
+        rho = 1.0 / (2.0 * sigma - rho_old)
+        coefs.append((rho * rho_old, 2.0 * rho / delta))
+        rho_old = rho
+    return theta, coefs
+
+
+def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings, steps: int, x_zero: bool):
+    """In-place restarted Chebyshev on device buffers (multigrid.py:176-205)."""
+    theta, coefs = _cheb_coeffs(lam_max, s)
+    n = x.numel()
+    L = lib()
+    for step in range(steps):
+        zero = x_zero and step == 0
+        if not zero:
+            _apply_into(apply_fn, x, ax)
+        check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None if zero else dv.ptr(ax), dv.ptr(inv_d), 1,
+                             theta, 0.0, 0.0, int(zero), None, dv.stream()))
+        for cd, cz in coefs:
+            _apply_into(apply_fn, x, ax)
+            check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), dv.ptr(ax), dv.ptr(inv_d), 0, 0.0, cd, cz, 0,
+                                 None, dv.stream()))
+    return x
+
+
+def chebyshev_apply(apply_fn, inv_diagonal, lam_max: float, b, x, settings: ChebyshevSettings = ChebyshevSettings(),
+                    steps: int = 1):
+    """Chebyshev semi-iteration targeting [lo, hi] lam_max of D^-1 A (multigrid.py:176-205)."""
+    bd = dv.as_dev(b)
+    xd = dv.as_dev(x).clone()
+    invd = dv.as_dev(inv_diagonal)
+    d = torch.empty_like(xd)
+    ax = torch.empty_like(xd)
+    _chebyshev_into(apply_fn, invd, lam_max, bd, xd, d, ax, settings, steps, False)
+    return dv.like_input(xd, x)
+
+
+class LevelOperator:
+    """Tangent of one level plus its smoother data (multigrid.py:208-252)."""
+
+    def __init__(self, problem: Problem, u_level, strategy: str, seed: int, level: int, is_coarsest: bool = False):
+        self.level = level
+        self.problem = problem
+        try:
+            self.op = MatrixFreeTangent(problem, u_level, strategy)
+        except NonPositiveJacobian as err:
+            raise NonPositiveJacobian(f"level {level}: {err}", element=err.element, level=level) from err
+        self.diag = self.op.diagonal()
+        self.inv_diag = torch.reciprocal(self.diag)
+        mask = problem.constraints.mask
+        self.lam_min, self.lam_max = estimate_eigenvalue_range(self.op, self.diag, seed=seed, constrained=mask)
+        if is_coarsest:
+            lo, _ = estimate_eigenvalue_range(self.op, self.diag, seed=seed, iterations=min(problem.n_dofs, 120),
+                                              constrained=mask)
+            self.lam_min = min(self.lam_min, lo)
+        self._cap_warned = False
+        n = problem.n_dofs
+        # per-level V-cycle buffers
+        self.b = torch.zeros(n, dtype=torch.float64, device="cuda")
+        self.x = torch.zeros_like(self.b)
+        self.d = torch.zeros_like(self.b)
+        self.ax = torch.zeros_like(self.b)
+        self.r = torch.zeros_like(self.b)
+        self.scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+        self.flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def smooth(self, b, x, steps: int, settings: ChebyshevSettings):
+        return chebyshev_apply(self.op, self.inv_diag, self.lam_max, b, x, settings, steps)
+
+    def smooth_into(self, b, x, steps, settings, x_zero=False):
+        return _chebyshev_into(self.op, self.inv_diag, self.lam_max, b, x, self.d, self.ax, settings, steps, x_zero)
+
+    def coarse_settings(self, settings: ChebyshevSettings) -> ChebyshevSettings:
+        """Range widened to the estimated smallest eigenvalue (multigrid.py:248-252)."""
+        lo = max(0.5 * self.lam_min / self.lam_max, 1e-8)
+        return ChebyshevSettings(degree=settings.degree, range_lo=min(lo, settings.range_lo),
+                                 range_hi=settings.range_hi)
+
+    def cap_reached(self) -> bool:
+        """Whether the last coarse solve hit the application cap (reads the device flag)."""
+        return int(self.flag.item()) == 0
+
+
+def _coarse_solve_into(level: LevelOperator, b, x, rel_target=1e-3, max_applications=100,
+                       settings: ChebyshevSettings = ChebyshevSettings()):
+    """Graph-capturable continuous Chebyshev coarse solve (multigrid.py:255-306).
+
+    The ||r|| test every ``degree`` applications runs on the device and raises
+    ``level.flag``; later kernels see the flag and do nothing, which returns
+    the same iterate as the reference's early ``return``."""
+    s = level.coarse_settings(settings)
+    theta = 0.5 * (s.range_hi + s.range_lo) * level.lam_max
+    delta = 0.5 * (s.range_hi - s.range_lo) * level.lam_max
+    sigma = theta / delta
+    n = b.numel()
+    L = lib()
+    ws = dv.Workspace.get().handle
+    scal, flag, d, ax = level.scal, level.flag, level.d, level.ax
+    # scal[0] = ||b||^2, scal[1] = rel_target * ||b||, flag = (||b|| == 0)
+    dv.dot(b, b, scal[0:1])
+    check(L.hf_scalar_op(1, dv.ptr(scal), 0, 1, rel_target, dv.ptr(flag), dv.stream()))
+    # x = 0 + inv_d b / theta
+    check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None, dv.ptr(level.inv_diag), 1, theta, 0.0, 0.0, 1,
+                         None, dv.stream()))
+    rho_old = 1.0 / sigma
+    for step in range(2, max_applications + 1):
+        level.op.apply_into(x, ax, flag)
+        if step % s.degree == 0:
+            check(L.hf_resnorm_check(ws, n, dv.ptr(b), dv.ptr(ax), dv.ptr(scal), 2, 1, dv.ptr(flag), dv.stream()))
+        rho = 1.0 / (2.0 * sigma - rho_old)
+        check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), dv.ptr(ax), dv.ptr(level.inv_diag), 0, 0.0,
+                             rho * rho_old, 2.0 * rho / delta, 0, dv.ptr(flag), dv.stream()))
+        rho_old = rho
+    return x
+
+
+def coarse_solve(level: LevelOperator, b, rel_target: float = 1e-3, max_applications: int = 100,
+                 settings: ChebyshevSettings = ChebyshevSettings()):
+    """Chebyshev iteration as coarse solver (multigrid.py:255-306)."""
+    bd = dv.as_dev(b)
+    x = torch.empty_like(bd)
+    _coarse_solve_into(level, bd, x, rel_target, max_applications, settings)
+    if level.cap_reached() and not level._cap_warned:
+        log.warning("coarse solve on level %d reached the application cap (%d); iterates remain usable "
+                    "(message shown once per level)", level.level, max_applications)
+        level._cap_warned = True
+    return dv.like_input(x, b)
+
+
+def _v_cycle_into(levels, transfers, b, x, lvl, steps, settings):
+    if lvl == 0:
+        return _coarse_solve_into(levels[0], b, x, settings=settings)
+    L = levels[lvl]
+    C = levels[lvl - 1]
+    L.smooth_into(b, x, steps, settings, x_zero=True)
+    L.op.apply_into(x, L.ax)
+    check(lib().hf_resid_masked(b.numel(), dv.ptr(L.r), dv.ptr(b), dv.ptr(L.ax), L.problem.mask_ptr(), dv.stream()))
+    transfers[lvl - 1].restrict_into(L.r, C.b, mode=1)
+    _v_cycle_into(levels, transfers, C.b, C.x, lvl - 1, steps, settings)
+    transfers[lvl - 1].prolong_into(C.x, x, mode=2)
+    L.smooth_into(b, x, steps, settings, x_zero=False)
+    return x
+
+
+def v_cycle(levels, transfers, b, lvl=None, smoothing_steps: int = 2,
+            settings: ChebyshevSettings = ChebyshevSettings()):
+    """One V-cycle (multigrid.py:309-332)."""
+    if lvl is None:
+        lvl = len(levels) - 1
+    bd = dv.as_dev(b)
+    x = torch.empty_like(bd)
+    _v_cycle_into(levels, transfers, bd, x, lvl, smoothing_steps, settings)
+    return dv.like_input(x, b)
+
+
+class GMGPreconditioner:
+    """V-cycle preconditioner (multigrid.py:335-351), replayed as one CUDA graph."""
+
+    def __init__(self, levels, transfers, smoothing_steps: int = 2, settings: ChebyshevSettings = ChebyshevSettings(),
+                 use_graph: bool = True):
+        self.levels = levels
+        self.transfers = transfers
+        self.smoothing_steps = smoothing_steps
+        self.settings = settings
+        self.use_graph = use_graph
+        self._graph = None
+        fine = levels[-1]
+        self._b = fine.b if len(levels) > 1 else torch.zeros_like(fine.b)
+        self._x = fine.x if len(levels) > 1 else torch.zeros_like(fine.b)
+
+    def _run(self):
+        _v_cycle_into(self.levels, self.transfers, self._b, self._x, len(self.levels) - 1, self.smoothing_steps,
+                      self.settings)
+
+    def apply_into(self, b: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        self._b.copy_(b)
+        if not self.use_graph:
+            self._run()
+        else:
+            if self._graph is None:
+                self._run()  # eager warm-up, then capture the identical launch sequence
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._run()
+                self._graph = g
+                self._b.copy_(b)
+            self._graph.replay()
+        out.copy_(self._x)
+        return out
+
+    def apply(self, b):
+        bd = dv.as_dev(b)
+        out = torch.empty_like(bd)
+        self.apply_into(bd, out)
+        return dv.like_input(out, b)
+
+    def __call__(self, b):
+        return self.apply(b)
+
+
+def build_transfers(problems):
+    return [TransferOperator(problems[i], problems[i + 1]) for i in range(len(problems) - 1)]
+
+
+def build_level_operators(problems, u_fine, strategy: str = "tensor4", seed: int = 0, keep_constrained: bool = False):
+    """Linearise every level at the injected fine displacement (multigrid.py:358-369)."""
+    u_levels = restrict_solution(problems, dv.as_dev(u_fine), keep_constrained)
+    return [LevelOperator(p, u, strategy, seed=seed + 7919 * lvl, level=lvl, is_coarsest=(lvl == 0))
+            for lvl, (p, u) in enumerate(zip(problems, u_levels))]
+
+
+def build_gmg(problems, u_fine, strategy: str = "tensor4", seed: int = 0, transfers=None,
+              keep_constrained: bool = False, use_graph: bool = True) -> GMGPreconditioner:
+    """(multigrid.py:372-382)"""
+    if transfers is None:
+        transfers = build_transfers(problems)
+    levels = build_level_operators(problems, u_fine, strategy, seed, keep_constrained)
+    return GMGPreconditioner(levels, transfers, use_graph=use_graph)

@@ -1,0 +1,337 @@
+"""Problem, matrix-free tangent and residual on the B200 (reference operators.py).
+
+Host objects keep the reference API (operators.py:83-116, 205-224, 319-417,
+519-522); every numeric step runs in libhf.so:
+
+* ``Problem``         -> ``hf_space``   (1D tables, lattice, J^-1/JxW computed on device)
+* ``MatrixFreeTangent``-> ``hf_tangent``(q-point caches built on device; apply/diagonal kernels)
+* ``compute_residual``-> ``hf_residual``
+
+Vectors may be numpy arrays (copied to/from the device around the call, the
+reference's calling convention) or CUDA fp64 torch tensors (stay on device).
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device as dv
+from ._lib import HF_ERR_JACOBIAN, STRATEGY_CODE, HfErrorInfo, check, lib
+from .fespace import (ConstraintSet, bottom_constraints, build_dof_map, gauss_legendre, lagrange_basis)
+from .material import NeoHookeanParams, NonPositiveJacobian, n_sym
+from .mesh import INCLUSION, Mesh, MeshHierarchy, lex_grid_indices, lex_grid_points
+
+STRATEGIES = ("scalar", "tensor2", "tensor4")
+
+
+@dataclass(frozen=True)
+class Material:
+    """Two-phase material (operators.py:75-80)."""
+
+    matrix: NeoHookeanParams
+    inclusion: NeoHookeanParams
+
+
+@dataclass(frozen=True)
+class GeometryCache:
+    """Host copy of the device geometry (mesh.py:117-130)."""
+
+    jac_inv: np.ndarray  # (n_el, nq, dim, dim)
+    jxw: np.ndarray  # (n_el, nq)
+
+    @property
+    def nbytes(self) -> int:
+        return self.jac_inv.nbytes + self.jxw.nbytes
+
+
+class Problem:
+    """One discretisation level (operators.py:83-116), resident on the GPU."""
+
+    def __init__(self, mesh: Mesh, degree: int, mat: Material, n_qpoints: int | None = None,
+                 basis_nodes: str = "equispaced", has_top_face: bool = True):
+        dv.require_cuda()
+        self.mesh = mesh
+        self.degree = degree
+        self.quadrature = gauss_legendre(n_qpoints if n_qpoints is not None else degree + 1)
+        self.basis = lagrange_basis(degree, self.quadrature, nodes=basis_nodes)
+        self.dofmap = build_dof_map(mesh, degree, components=mesh.dim)
+        self.material = mat
+        inc = mesh.material_id == INCLUSION
+        self.mu_el = np.where(inc, mat.inclusion.mu, mat.matrix.mu)[:, None]
+        self.lam_el = np.where(inc, mat.inclusion.lam, mat.matrix.lam)[:, None]
+        self.has_top_face = has_top_face
+        self._constraints = bottom_constraints(mesh, self.dofmap)
+        q = self.quadrature.n_points
+        cells = (ct.c_int * 3)(*(list(mesh.cells) + [1] * (3 - mesh.dim)))
+        h = ct.c_void_p()
+        vals = np.ascontiguousarray(self.basis.values)
+        ders = np.ascontiguousarray(self.basis.derivatives)
+        verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+        mu = np.ascontiguousarray(self.mu_el[:, 0])
+        lam = np.ascontiguousarray(self.lam_el[:, 0])
+        mask = np.ascontiguousarray(self._constraints.mask.astype(np.uint8))
+        rc = lib().hf_space_create(mesh.dim, degree, q, cells, vals.ctypes.data, ders.ctypes.data,
+                                   self.quadrature.points.ctypes.data, self.quadrature.weights.ctypes.data,
+                                   verts.ctypes.data, mu.ctypes.data, lam.ctypes.data, mask.ctypes.data,
+                                   dv.stream(), ct.byref(h))
+        if rc == 5:
+            raise ValueError(lib().hf_last_error().decode())
+        check(rc)
+        self._space = h
+        self._geometry = None
+        self._sw = None
+        self._sw_dev = None
+        self._mask_dev = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "_space", None):
+                lib().hf_space_destroy(self._space)
+                self._space = None
+        except Exception:
+            pass
+
+    # --- reference attributes
+    @property
+    def dim(self) -> int:
+        return self.mesh.dim
+
+    @property
+    def n_dofs(self) -> int:
+        return self.dofmap.n_dofs
+
+    @property
+    def n_qpoints_per_cell(self) -> int:
+        return self.quadrature.n_points ** self.dim
+
+    def zero_vector(self) -> np.ndarray:
+        return np.zeros(self.n_dofs)
+
+    @property
+    def constraints(self) -> ConstraintSet:
+        return self._constraints
+
+    @constraints.setter
+    def constraints(self, cs: ConstraintSet) -> None:
+        if cs.n_dofs != self.n_dofs:
+            raise ValueError("constraint set does not match the DoF count")
+        self._constraints = cs
+        m = np.ascontiguousarray(cs.mask.astype(np.uint8))
+        check(lib().hf_space_set_mask(self._space, m.ctypes.data, dv.stream()))
+        self._mask_dev = None
+
+    @property
+    def mask_dev(self) -> torch.Tensor:
+        """Device bool mask (torch) of the constrained DoFs."""
+        if self._mask_dev is None:
+            self._mask_dev = torch.from_numpy(self._constraints.mask.copy()).to("cuda")
+        return self._mask_dev
+
+    def mask_ptr(self) -> ct.c_void_p:
+        m = ct.c_void_p()
+        check(lib().hf_space_pointers(self._space, None, None, ct.byref(m)))
+        return m
+
+    @property
+    def geometry(self) -> GeometryCache:
+        """Download J^-1 and JxW (computed on the device) in the reference layout."""
+        if self._geometry is None:
+            d, nel, nq = self.dim, self.mesh.n_elements, self.n_qpoints_per_cell
+            nqp = nel * nq
+            a = torch.empty(d * d * nqp, dtype=torch.float64, device="cuda")
+            b = torch.empty(nqp, dtype=torch.float64, device="cuda")
+            check(lib().hf_space_geometry_copy(self._space, dv.ptr(a), dv.ptr(b), dv.stream()))
+            jinv = a.cpu().numpy().reshape(d, d, nel, nq).transpose(2, 3, 0, 1).copy()
+            self._geometry = GeometryCache(jinv, b.cpu().numpy().reshape(nel, nq))
+        return self._geometry
+
+    @property
+    def surface_weights(self) -> np.ndarray:
+        if self._sw is None:
+            self._sw = top_surface_weights(self) if self.has_top_face else np.zeros(self.dofmap.n_nodes)
+        return self._sw
+
+    @property
+    def surface_weights_dev(self) -> torch.Tensor:
+        if self._sw_dev is None:
+            self._sw_dev = dv.as_dev(self.surface_weights)
+        return self._sw_dev
+
+
+def build_problem_hierarchy(hierarchy: MeshHierarchy, degree: int, mat: Material, n_qpoints: int | None = None):
+    """One Problem per mesh level, coarsest first (operators.py:119-126)."""
+    return [Problem(m, degree, mat, n_qpoints=n_qpoints) for m in hierarchy.levels]
+
+
+def top_surface_weights(problem: Problem) -> np.ndarray:
+    """s_n = int_top N_n dS per lattice node (operators.py:129-167); host setup."""
+    mesh, basis = problem.mesh, problem.basis
+    d = mesh.dim
+    fd = d - 1
+    surf = np.zeros(problem.dofmap.n_nodes)
+    e = lex_grid_indices(mesh.cells)
+    top = np.flatnonzero(e[:, d - 1] == mesh.cells[d - 1] - 1)
+    if len(top) == 0:
+        return surf
+    quad = basis.quadrature
+    pts = lex_grid_points([quad.points] * fd)
+    wts = lex_grid_points([quad.weights] * fd).prod(axis=1)
+    off = lex_grid_indices((2,) * d)
+    fc = np.flatnonzero(off[:, d - 1] == 1)
+    corners = mesh.element_corners()[top][:, fc]
+    foff = lex_grid_indices((2,) * fd)
+    dn = np.ones((2**fd, len(pts), fd))
+    for k in range(fd):
+        fac = np.where(foff[:, k : k + 1] == 1, pts[None, :, k], 1.0 - pts[None, :, k])
+        dfac = np.where(foff[:, k : k + 1] == 1, 1.0, -1.0)
+        for a in range(fd):
+            dn[:, :, a] *= dfac if a == k else fac
+    tang = np.einsum("fci,cqk->fqik", corners, dn)
+    if d == 2:
+        ds = np.linalg.norm(tang[..., 0], axis=-1)
+    else:
+        ds = np.linalg.norm(np.cross(tang[..., 0], tang[..., 1]), axis=-1)
+    n1 = basis.n_nodes_1d
+    nm = lex_grid_indices((n1,) * fd)
+    qm = lex_grid_indices((quad.n_points,) * fd)
+    nface = np.ones((n1**fd, quad.n_points**fd))
+    for k in range(fd):
+        nface *= basis.values[nm[:, k][:, None], qm[:, k][None, :]]
+    local = np.einsum("nq,fq->fn", nface, wts[None, :] * ds)
+    # top-face lattice nodes of each top cell (local last index = p)
+    npa = problem.dofmap.nodes_per_axis
+    p = problem.degree
+    strides = np.cumprod((1,) + npa[:-1])
+    loc = lex_grid_indices((n1,) * fd)
+    base = e[top] * p
+    nodes = np.zeros((len(top), n1**fd), dtype=np.int64)
+    for a in range(fd):
+        nodes += (base[:, a][:, None] + loc[None, :, a]) * strides[a]
+    nodes += (base[:, d - 1][:, None] + p) * strides[d - 1]
+    np.add.at(surf, nodes, local)
+    return surf
+
+
+# ---------------------------------------------------------------------------
+
+
+def _raise_jacobian(err: HfErrorInfo, level=None):
+    raise NonPositiveJacobian(lib().hf_last_error().decode(), element=int(err.element), level=level)
+
+
+def jacobian_range(problem: Problem, u) -> tuple[float, float]:
+    """Min and max of det F over all quadrature points (operators.py:192-196)."""
+    ud = dv.as_dev(u)
+    lo, hi = ct.c_double(), ct.c_double()
+    check(lib().hf_jacobian_range(problem._space, dv.ptr(ud), dv.stream(), ct.byref(lo), ct.byref(hi), None, None))
+    return lo.value, hi.value
+
+
+def compute_residual(problem: Problem, u, traction=None):
+    """Internal Kirchhoff-stress force minus the top traction, constrained
+    entries zeroed (operators.py:205-224)."""
+    ud = dv.as_dev(u)
+    out = torch.empty_like(ud)
+    err = HfErrorInfo()
+    if traction is not None:
+        t = np.ascontiguousarray(np.asarray(traction, dtype=np.float64).reshape(-1))
+        rc = lib().hf_residual(problem._space, dv.ptr(ud), t.ctypes.data, dv.ptr(problem.surface_weights_dev),
+                               dv.ptr(out), dv.stream(), ct.byref(err))
+    else:
+        rc = lib().hf_residual(problem._space, dv.ptr(ud), None, None, dv.ptr(out), dv.stream(), ct.byref(err))
+    if rc == HF_ERR_JACOBIAN:
+        _raise_jacobian(err)
+    check(rc)
+    return dv.like_input(out, u)
+
+
+@dataclass
+class CacheInfo:
+    """What the reference exposes of its quadrature caches (operators.py:244-289)."""
+
+    strategy: str
+    payload_scalars_per_qpoint: int
+    payload_nbytes: int
+
+
+class MatrixFreeTangent:
+    """Apply-only tangent backed by one of the three q-point caches (operators.py:319-417)."""
+
+    def __init__(self, problem: Problem, u_bar, strategy: str = "tensor4"):
+        if strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {strategy!r}")
+        self.problem = problem
+        self.strategy = strategy
+        ud = dv.as_dev(u_bar)
+        h = ct.c_void_p()
+        err = HfErrorInfo()
+        rc = lib().hf_tangent_create(problem._space, STRATEGY_CODE[strategy], dv.ptr(ud), dv.stream(), ct.byref(h),
+                                     ct.byref(err))
+        if rc == HF_ERR_JACOBIAN:
+            _raise_jacobian(err)
+        check(rc)
+        self._op = h
+        sb, ps, pb = ct.c_longlong(), ct.c_int(), ct.c_longlong()
+        check(lib().hf_tangent_storage(h, ct.byref(sb), ct.byref(ps), ct.byref(pb)))
+        self._storage = sb.value
+        self.cache = CacheInfo(strategy, ps.value, pb.value)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_op", None):
+                lib().hf_tangent_destroy(self._op)
+                self._op = None
+        except Exception:
+            pass
+
+    @property
+    def n_dofs(self) -> int:
+        return self.problem.n_dofs
+
+    def apply_into(self, x: torch.Tensor, y: torch.Tensor, skip: torch.Tensor | None = None) -> torch.Tensor:
+        """y = A x on device buffers (no allocation; graph-capturable)."""
+        check(lib().hf_tangent_apply_flagged(self._op, dv.ptr(x), dv.ptr(y), dv.ptr(skip), dv.stream()))
+        return y
+
+    def apply_raw(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+        """y += sum over cells of A_loc x (constrained rows dropped), no init."""
+        check(lib().hf_tangent_apply_raw(self._op, dv.ptr(x), dv.ptr(y), None, dv.stream()))
+        return y
+
+    def apply(self, x, out=None):
+        """y = A x: zero-in / identity-out on the constrained subspace (operators.py:331-339).
+
+        numpy in -> numpy out; CUDA tensor in -> CUDA tensor out; a (pinned)
+        CPU tensor ``out`` receives the result through an async D2H copy."""
+        xd = dv.as_dev(x)
+        y = torch.empty_like(xd)
+        self.apply_into(xd, y)
+        if out is not None:
+            out.copy_(y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return out
+        return dv.like_input(y, x)
+
+    def __call__(self, x):
+        return self.apply(x)
+
+    def diagonal(self, as_numpy: bool | None = None):
+        """diag(A), constrained entries 1 (operators.py:395-410)."""
+        d = torch.empty(self.n_dofs, dtype=torch.float64, device="cuda")
+        check(lib().hf_tangent_diagonal(self._op, dv.ptr(d), dv.stream()))
+        return d.cpu().numpy() if as_numpy else d
+
+    def storage_bytes(self) -> int:
+        """Strategy payload plus geometry (operators.py:412-417)."""
+        return self._storage
+
+
+def make_tangent(problem: Problem, u_bar, strategy: str):
+    """(operators.py:519-522).  The CSR "matrix_based" baseline is a SURVEY §8(f) next row."""
+    if strategy == "matrix_based":
+        raise NotImplementedError("matrix_based (CSR) tangent is not part of the B200 hot path yet")
+    return MatrixFreeTangent(problem, u_bar, strategy)

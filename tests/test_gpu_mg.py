@@ -1,0 +1,115 @@
+"""GPU parity of the multigrid/CG path against the reference golden runs:
+transfers, injection, Lanczos range, Chebyshev, coarse solve, V-cycle, GMG-CG."""
+
+import numpy as np
+import pytest
+
+from _cases import golden, product_levels, rel
+
+pytestmark = pytest.mark.gpu
+MG = ["mg_2d_16.npz", "mg_3d_8.npz", "mg_2d_32_cfg1.npz"]
+
+
+@pytest.fixture(scope="module", params=MG)
+def case(request):
+    from paper_1904_13131_b200 import build_gmg, build_transfers
+
+    g = golden(request.param)
+    probs = product_levels(g)
+    for i, p in enumerate(probs):
+        assert np.array_equal(p.mu_el[:, 0], g[f"mu_{i}"]), "per-level centroid material differs"
+    transfers = build_transfers(probs)
+    gmg = build_gmg(probs, g["ubar"], str(g["strategy"]), seed=0, transfers=transfers)
+    return g, probs, transfers, gmg
+
+
+def test_transfers(case):
+    g, probs, transfers, _ = case
+    for i, t in enumerate(transfers):
+        assert rel(t.prolong(g[f"prolong_in_{i}"]), g[f"prolong_out_{i}"]) < 1e-14
+        assert rel(t.restrict(g[f"restrict_in_{i}"]), g[f"restrict_out_{i}"]) < 1e-14
+
+
+def test_injection(case):
+    from paper_1904_13131_b200 import restrict_solution
+
+    g, probs, _, _ = case
+    for i, v in enumerate(restrict_solution(probs, g["ubar"])):
+        assert np.array_equal(v, g[f"inject_{i}"])
+
+
+def test_level_setup(case):
+    g, probs, _, gmg = case
+    for i, lv in enumerate(gmg.levels):
+        assert rel(lv.diag.cpu().numpy(), g[f"diag_{i}"]) < 1e-12
+        assert abs(lv.lam_max - float(g[f"lam_max_{i}"])) <= 1e-9 * abs(float(g[f"lam_max_{i}"]))
+        assert abs(lv.lam_min - float(g[f"lam_min_{i}"])) <= 1e-6 * abs(float(g[f"lam_min_{i}"]))
+
+
+def test_chebyshev_and_coarse(case):
+    from paper_1904_13131_b200 import ChebyshevSettings, chebyshev_apply, coarse_solve
+
+    g, probs, _, gmg = case
+    lv = gmg.levels[-1]
+    out = chebyshev_apply(lv.op, lv.inv_diag, lv.lam_max, g["b"], g["cheb_x0"], ChebyshevSettings(), 2)
+    assert rel(out, g["cheb_out"]) < 1e-10
+    assert rel(coarse_solve(gmg.levels[0], g["coarse_b"]), g["coarse_out"]) < 1e-8
+
+
+def test_vcycle(case):
+    g, probs, _, gmg = case
+    z = gmg.apply(g["b"])
+    assert rel(z, g["vcycle"]) < 1e-8
+    z2 = gmg.apply(g["b"])  # graph replay gives the same result
+    assert rel(z2, z) < 1e-13
+
+
+def test_gmg_cg(case):
+    from paper_1904_13131_b200 import MatrixFreeTangent, cg
+
+    g, probs, _, gmg = case
+    op = MatrixFreeTangent(probs[-1], g["ubar"], str(g["strategy"]))
+    x, rep = cg(op, g["b"], rel_tol=1e-8, preconditioner=gmg)
+    assert abs(rep.iterations - int(g["cg_iterations"])) <= 1
+    assert rel(x, g["cg_solution"]) < 1e-6
+    h = np.array(rep.residual_history)
+    k = min(len(h), len(g["cg_history"]))
+    assert np.allclose(h[:k], g["cg_history"][:k], rtol=1e-5)
+
+
+def test_newton_traction_reference():
+    """The reference's own newton_solve (traction) on a tiny 2D problem."""
+    from paper_1904_13131_b200 import LoadSpec, NewtonSettings, newton_solve
+
+    g = golden("newton_traction_2d.npz")
+    g["dim"] = 2
+    probs = product_levels(g)
+    res = newton_solve(probs, NewtonSettings(n_load_steps=int(g["n_steps"])),
+                       LoadSpec(float(g["magnitude"]), tuple(g["direction"])), "gmg", "tensor4", seed=0)
+    recs = np.array([(r.load_step, r.fraction, r.iteration, r.residual_norm, r.update_norm, r.cg_iterations)
+                     for r in res.records])
+    ref = g["records"]
+    assert recs.shape == ref.shape
+    assert np.array_equal(recs[:, [0, 2]], ref[:, [0, 2]])
+    assert np.all(np.abs(recs[:, 5] - ref[:, 5]) <= 1)
+    big = ref[:, 3] > 1e-9
+    assert np.allclose(recs[big, 3], ref[big, 3], rtol=1e-4)
+    assert rel(res.u.cpu().numpy(), g["u"]) < 1e-8
+
+
+def test_newton_prescribed_golden():
+    """Config-4 restatement (prescribed top displacement) vs the
+    golden run driven by reference primitives (tests/golden/make_golden.py)."""
+    from paper_1904_13131_b200 import NewtonSettings, newton_solve_prescribed
+
+    g = golden("newton_prescribed_3d.npz")
+    g["dim"] = 3
+    probs = product_levels(g)
+    res = newton_solve_prescribed(probs, NewtonSettings(n_load_steps=int(g["n_steps"])), float(g["target"]))
+    recs = np.array([(r.load_step, r.iteration, r.residual_norm, r.update_norm, r.cg_iterations) for r in res.records])
+    ref = g["records"]
+    assert recs.shape == ref.shape
+    assert np.array_equal(recs[:, :2], ref[:, :2])
+    assert np.all(np.abs(recs[:, 4] - ref[:, 4]) <= 1)
+    assert np.allclose(recs[:, 2], ref[:, 2], rtol=1e-3, atol=1e-11)
+    assert rel(res.u.cpu().numpy(), g["u"]) < 1e-8
