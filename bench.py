@@ -258,7 +258,7 @@ def run_ours(args):
                        "l2": "256 MiB flush before every timed step", "parallelism": f"replicas x{ws}"},
             "roofline": {"bound": "hbm", "achieved": ab / kern_ms / 1e6, "peak": hbm, "unit": "GB/s",
                          "frac": ab / kern_ms / 1e6 / hbm, "traffic": None, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": ab, "kernel": "hf::k_apply<3,3,TENSOR4>"},
+                         "algorithmic_bytes_per_launch": ab, "kernel": "hf::k_apply_line<3,3,TENSOR4>"},
             "e2e": {"value": ws * p.n_dofs / e2e_ms / 1e6, "unit": "GDoF/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches, "clocks": clocks, "variants": variants}

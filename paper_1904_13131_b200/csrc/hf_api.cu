@@ -79,6 +79,7 @@ struct hf_space {
   double* d_mu = nullptr;
   double* d_lam = nullptr;
   uint8_t* d_mask = nullptr;
+  uint32_t* d_lmask = nullptr;  // per (cell, last-axis line): constraint bits (k_line_masks)
   unsigned long long* d_u64 = nullptr;  // [0] detmin [1] detmax [2] first-index
 };
 
@@ -108,6 +109,13 @@ struct hf_ws {
   double* d_partials = nullptr;
   unsigned* d_counter = nullptr;
 };
+
+static cudaError_t update_cell_flags(hf_space* sp, cudaStream_t s) {
+  if (sp->lat.n_el <= 0) return cudaSuccess;
+  const long long n = sp->lat.n_el * (sp->dim == 3 ? sp->n1 * sp->n1 : sp->n1);
+  k_line_masks<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sp->lat, sp->dim, sp->degree, sp->d_mask, sp->d_lmask);
+  return cudaGetLastError();
+}
 
 extern "C" {
 
@@ -186,12 +194,14 @@ HF_API int hf_space_create(int dim, int degree, int nq1, const int* cells, const
   ALLOC(sp->d_mu, sizeof(double) * nel);
   ALLOC(sp->d_lam, sizeof(double) * nel);
   ALLOC(sp->d_mask, sp->n_dofs);
+  ALLOC(sp->d_lmask, sizeof(uint32_t) * (nel > 0 ? nel : 1) * (dim == 3 ? N * N : N));
   ALLOC(sp->d_u64, sizeof(unsigned long long) * 4);
   ALLOC(d_verts, sizeof(double) * nverts * dim);
   HF_CUDA(cudaMemcpyAsync(d_verts, vertices, sizeof(double) * nverts * dim, cudaMemcpyHostToDevice, s));
   HF_CUDA(cudaMemcpyAsync(sp->d_mu, mu_el, sizeof(double) * nel, cudaMemcpyHostToDevice, s));
   HF_CUDA(cudaMemcpyAsync(sp->d_lam, lam_el, sizeof(double) * nel, cudaMemcpyHostToDevice, s));
   HF_CUDA(cudaMemcpyAsync(sp->d_mask, mask, sp->n_dofs, cudaMemcpyHostToDevice, s));
+  HF_CUDA(update_cell_flags(sp, s));
   unsigned long long init = ~0ull;
   HF_CUDA(cudaMemcpyAsync(sp->d_u64, &init, sizeof(init), cudaMemcpyHostToDevice, s));
   HF_CUDA(launch_geometry(dim, sp->tab, sp->lat, N, d_verts, sp->d_jinv, sp->d_jxw, sp->d_u64, s));
@@ -212,6 +222,7 @@ HF_API int hf_space_create(int dim, int degree, int nq1, const int* cells, const
 HF_API int hf_space_set_mask(hf_space* sp, const unsigned char* mask, void* stream) {
   if (!sp || !mask) return fail(HF_ERR_ARG, "null argument");
   HF_CUDA(cudaMemcpyAsync(sp->d_mask, mask, sp->n_dofs, cudaMemcpyHostToDevice, S(stream)));
+  HF_CUDA(update_cell_flags(sp, S(stream)));
   HF_CUDA(cudaStreamSynchronize(S(stream)));
   return HF_OK;
 }
@@ -249,6 +260,7 @@ HF_API int hf_space_destroy(hf_space* sp) {
   cudaFree(sp->d_mu);
   cudaFree(sp->d_lam);
   cudaFree(sp->d_mask);
+  cudaFree(sp->d_lmask);
   cudaFree(sp->d_u64);
   delete sp;
   return HF_OK;
@@ -266,6 +278,7 @@ static CellArgs base_args(const hf_space* sp) {
   a.mu = sp->d_mu;
   a.lam = sp->d_lam;
   a.mask = sp->d_mask;
+  a.lmask = sp->d_lmask;
   return a;
 }
 
@@ -279,7 +292,7 @@ static int nfields(int dim, int strategy) {
   int nv = dim * (dim + 1) / 2, nm = nv * (nv + 1) / 2;
   if (strategy == HF_TENSOR4) return nv + nm + dim * dim + 1;
   if (strategy == HF_TENSOR2) return 2 + nv + dim * dim + 1;
-  return 1;
+  return 2 + dim * dim;  // c1 + J^-1 + JxW (tile layout, hf_line.cuh)
 }
 
 // locate the first q-point (flat e*nq+q) attaining min det F of state u
@@ -340,7 +353,8 @@ HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev,
   op->sp = sp;
   op->strategy = strategy;
   op->nf = nfields(sp->dim, strategy);
-  HF_CUDA(cudaMalloc((void**)&op->d_cache, sizeof(double) * op->nf * (sp->lat.n_qp > 0 ? sp->lat.n_qp : 1)));
+  const long long ncache = tile_cache_doubles(sp->dim, sp->n1, op->nf, sp->lat.n_el);
+  HF_CUDA(cudaMalloc((void**)&op->d_cache, sizeof(double) * (ncache > 0 ? ncache : 1)));
   if (strategy == HF_SCALAR) {
     HF_CUDA(cudaMalloc((void**)&op->d_ubar, sizeof(double) * sp->n_dofs));
     HF_CUDA(cudaMemcpyAsync(op->d_ubar, ubar_dev, sizeof(double) * sp->n_dofs, cudaMemcpyDeviceToDevice, s));

@@ -43,8 +43,10 @@ template <int DIM, int VAR>
 struct CacheFields {
   static constexpr int NV = DIM * (DIM + 1) / 2;
   static constexpr int NM = NV * (NV + 1) / 2;
-  // tensor4: tau(NV) M(NM) sinv(D*D) JxW ; tensor2: c1 c2 tau(NV) sinv JxW ; scalar: c1
-  static constexpr int NF = VAR == TENSOR4 ? NV + NM + DIM * DIM + 1 : (VAR == TENSOR2 ? 2 + NV + DIM * DIM + 1 : 1);
+  // tensor4: tau(NV) M(NM) sinv(D*D) JxW ; tensor2: c1 c2 tau(NV) sinv JxW ;
+  // scalar: c1 J^-1(D*D) JxW (the geometry it re-reads, stored beside c1 in the tile layout)
+  static constexpr int NF = VAR == TENSOR4 ? NV + NM + DIM * DIM + 1
+                                           : (VAR == TENSOR2 ? 2 + NV + DIM * DIM + 1 : 2 + DIM * DIM);
 };
 
 struct CellArgs {
@@ -61,6 +63,7 @@ struct CellArgs {
   const double* lam;        // [n_el]
   const double* ubar;       // scalar strategy: snapshot of the linearisation point
   const uint8_t* mask;      // [n_dofs] constrained DoFs
+  const uint32_t* lmask;    // [n_el * lines] constraint bits per last-axis line (k_line_masks)
   const int* skip;          // optional device flag; non-zero -> kernel is a no-op
   unsigned long long* detmin;  // ordered-double min of det F (build / residual / range)
   unsigned long long* detmax;
@@ -402,113 +405,6 @@ HF_DEV void gather_nodal(const double* __restrict__ v, const uint8_t* __restrict
 }
 
 // ---------------------------------------------------------------------------
-// apply: y += A_loc x  (constrained rows dropped, constrained inputs zeroed)
-// ---------------------------------------------------------------------------
-template <int DIM, int N, int VAR>
-__global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_apply(const CellArgs a) {
-  using K = Cfg<DIM, N>;
-  constexpr int NQ = K::NQ;
-  constexpr int NF = CacheFields<DIM, VAR>::NF;
-  constexpr int NV = K::NV;
-  if (a.skip && *a.skip) return;
-  extern __shared__ double sm[];
-  load_tables<DIM, N>(sm, a.tab, false);
-  Team t = make_team<DIM, N>(a.lat, a.degree);
-  double* A = sm + K::TAB + t.slot * K::SBUF;
-  double* B = A + K::CPB * K::SBUF;
-  double* Gs = sm + K::TAB + 2 * K::CPB * K::SBUF + t.slot * DIM * K::SBUF;
-  const long long qi = t.e * NQ + t.lq;
-
-  // issue the streaming cache loads first so they overlap the gather/evaluate
-  double cf[NF];
-  if (t.act) {
-#pragma unroll
-    for (int f = 0; f < NF; ++f) cf[f] = __ldcs(a.cache + f * a.lat.n_qp + qi);
-  }
-  double gub[DIM][DIM];
-  if (VAR == SCALAR) {
-    gather_nodal<DIM, N>(a.ubar, nullptr, t, A);
-    __syncthreads();
-    eval_gradients<DIM, N>(A, B, sm, t, gub);
-  }
-  gather_nodal<DIM, N>(a.x, a.mask, t, A);
-  __syncthreads();
-  double gu[DIM][DIM];
-  eval_gradients<DIM, N>(A, B, sm, t, gu);
-
-  double G[DIM][DIM];
-  if (t.act) {
-    if (VAR == TENSOR4) {
-      double sinv[DIM][DIM], tau[DIM][DIM];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i)
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-          tau[i][j] = cf[hf_slot<DIM>(i, j)];
-          sinv[i][j] = cf[NV + K::NM + i * DIM + j];
-        }
-      qp_action<DIM, true>(gu, sinv, tau, 0.0, 0.0, cf + NV, cf[NF - 1], G);
-    } else if (VAR == TENSOR2) {
-      double sinv[DIM][DIM], tau[DIM][DIM];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i)
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-          tau[i][j] = cf[2 + hf_slot<DIM>(i, j)];
-          sinv[i][j] = cf[2 + NV + i * DIM + j];
-        }
-      qp_action<DIM, false>(gu, sinv, tau, cf[0], cf[1], nullptr, cf[NF - 1], G);
-    } else {
-      double ji[DIM][DIM];
-      load_jinv<DIM>(a, qi, ji);
-      const double mu = __ldg(a.mu + t.e), lam = __ldg(a.lam + t.e);
-      // rebuild F, b, tau = mu b - c1 I, sinv from ubar (operators.py:349-363)
-      double F[DIM * DIM];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i)
-#pragma unroll
-        for (int Aa = 0; Aa < DIM; ++Aa) {
-          double s = (i == Aa) ? 1.0 : 0.0;
-#pragma unroll
-          for (int q = 0; q < DIM; ++q) s = fma(gub[i][q], ji[q][Aa], s);
-          F[i * DIM + Aa] = s;
-        }
-      const double c1 = cf[0];
-      double tau[DIM][DIM], sinv[DIM][DIM], Fi[DIM * DIM];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i)
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-          double b = 0.0;
-#pragma unroll
-          for (int Aa = 0; Aa < DIM; ++Aa) b = fma(F[i * DIM + Aa], F[j * DIM + Aa], b);
-          tau[i][j] = mu * b - (i == j ? c1 : 0.0);
-        }
-      hf_inv<DIM>(F, hf_det<DIM>(F), Fi);
-#pragma unroll
-      for (int q = 0; q < DIM; ++q)
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) {
-          double s = 0.0;
-#pragma unroll
-          for (int Aa = 0; Aa < DIM; ++Aa) s = fma(ji[q][Aa], Fi[Aa * DIM + j], s);
-          sinv[q][j] = s;
-        }
-      qp_action<DIM, false>(gu, sinv, tau, 2.0 * c1, 2.0 * lam, nullptr, __ldg(a.jxw + qi), G);
-    }
-  }
-  double yl[DIM];
-  integrate_gradients<DIM, N>(A, B, Gs, sm, t, G, yl);
-  if (t.act) {
-#pragma unroll
-    for (int c = 0; c < DIM; ++c) {
-      long long d = t.node * DIM + c;
-      if (!a.mask[d]) atomicAdd(a.y + d, yl[c]);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // cache build (operators.py:292-311); also records min det F
 // ---------------------------------------------------------------------------
 template <int DIM, int N, int VAR>
@@ -537,22 +433,29 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_build(const CellArgs a) {
   }
   warp_minmax_atomic(a.detmin, nullptr, t.act ? k.J : 0.0, t.act);
   if (!t.act) return;
-  const long long nqp = a.lat.n_qp;
-  double* o = a.cache_out + qi;
+  constexpr int NF = CacheFields<DIM, VAR>::NF;
+  using TL = TileLayout<DIM, N>;
+  double* o = a.cache_out;
+  auto put = [&](int f, double v) { o[TL::index(t.e, t.lq, f, NF)] = v; };
+  int f = 0;
   if (VAR == SCALAR) {
-    o[0] = k.c1;
+    put(f++, k.c1);
+#pragma unroll
+    for (int r = 0; r < DIM; ++r)
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) put(f++, ji[r][c]);
+    put(f++, __ldg(a.jxw + qi));
     return;
   }
-  int f = 0;
   if (VAR == TENSOR2) {
-    o[(f++) * nqp] = 2.0 * k.c1;
-    o[(f++) * nqp] = 2.0 * lam;
+    put(f++, 2.0 * k.c1);
+    put(f++, 2.0 * lam);
   }
 #pragma unroll
   for (int s = 0; s < NV; ++s) {
     int i = s < DIM ? s : (DIM == 2 ? 0 : (s == 3 ? 1 : 0));
     int j = s < DIM ? s : (DIM == 2 ? 1 : (s == 5 ? 1 : 2));
-    o[(f++) * nqp] = k.tau[i][j];
+    put(f++, k.tau[i][j]);
   }
   if (VAR == TENSOR4) {
     // Voigt matrix of J c (material.py:195-208), packed upper (218-222)
@@ -563,14 +466,14 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_build(const CellArgs a) {
         double v = 0.0;
         if (r < DIM && c < DIM) v = 2.0 * lam + (r == c ? 2.0 * k.c1 : 0.0);
         else if (r == c) v = k.c1;
-        o[(f++) * nqp] = v;
+        put(f++, v);
       }
   }
 #pragma unroll
   for (int r = 0; r < DIM; ++r)
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) o[(f++) * nqp] = k.sinv[r][c];
-  o[(f++) * nqp] = __ldg(a.jxw + qi);
+    for (int c = 0; c < DIM; ++c) put(f++, k.sinv[r][c]);
+  put(f++, __ldg(a.jxw + qi));
 }
 
 // ---------------------------------------------------------------------------
@@ -606,7 +509,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_diag(const CellArgs a) {
       const double mu = __ldg(a.mu + t.e), lam = __ldg(a.lam + t.e);
       Kin<DIM> k;
       kinematics<DIM>(gub, ji, mu, lam, k, true);
-      const double c1 = a.cache[qi];  // cached c1 (same value as k.c1)
+      const double c1 = a.cache[TileLayout<DIM, N>::index(t.e, t.lq, 0, NF)];  // cached c1 (same value as k.c1)
 #pragma unroll
       for (int i = 0; i < DIM; ++i)
 #pragma unroll
@@ -627,7 +530,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_diag(const CellArgs a) {
   } else if (t.act) {
     double cf[NF];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) cf[f] = a.cache[f * a.lat.n_qp + qi];
+    for (int f = 0; f < NF; ++f) cf[f] = a.cache[TileLayout<DIM, N>::index(t.e, t.lq, f, NF)];
     const int off = (VAR == TENSOR2) ? 2 : 0;
 #pragma unroll
     for (int i = 0; i < DIM; ++i)
@@ -819,7 +722,8 @@ template <int DIM>
 __global__ void k_geometry(const HfTables tab, const HfLattice lat, int nq1, const double* __restrict__ verts,
                            double* __restrict__ jinv, double* __restrict__ jxw, unsigned long long* detmin) {
   long long qi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (qi >= lat.n_qp) return;
+  const bool valid = qi < lat.n_qp;
+  if (!valid) qi = lat.n_qp - 1;  // idle lanes recompute the last point (keeps the warp reduction full)
   int nq = nq1 * nq1 * (DIM == 3 ? nq1 : 1);
   long long e = qi / nq;
   int lq = (int)(qi - e * nq);
@@ -859,13 +763,44 @@ __global__ void k_geometry(const HfTables tab, const HfLattice lat, int nq1, con
     }
   }
   double det = hf_det<DIM>(Jm);
-  hf_atomic_min_d(detmin, det);
+  warp_minmax_atomic(detmin, nullptr, det, true);
+  if (!valid) return;
   double Ji[DIM * DIM];
   hf_inv<DIM>(Jm, det, Ji);
 #pragma unroll
   for (int i = 0; i < DIM * DIM; ++i) jinv[i * lat.n_qp + qi] = Ji[i];
   double w = tab.qw[qx] * tab.qw[qy] * (DIM == 3 ? tab.qw[qz] : 1.0);
   jxw[qi] = det * w;
+}
+
+// Per (cell, last-axis line) constraint bits for the line kernels
+// (hf_line.cuh): bit c*N + l is set when DoF c of node l of line t is
+// constrained.  One coalesced 32-bit load per lane replaces N*DIM byte loads
+// and the data-dependent branch on them.
+static __global__ void k_line_masks(const HfLattice lat, int dim, int degree, const uint8_t* __restrict__ mask,
+                                    uint32_t* __restrict__ bits) {
+  const int n1 = degree + 1;
+  const int L = dim == 3 ? n1 * n1 : n1;
+  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= lat.n_el * L) return;
+  const long long e = id / L;
+  const int t = (int)(id - e * L);
+  long long r = e;
+  const int ex = (int)(r % lat.cells[0]);
+  r /= lat.cells[0];
+  const int ey = (int)(r % lat.cells[1]);
+  const int ez = dim == 3 ? (int)(r / lat.cells[1]) : 0;
+  const int i = t % n1, j = dim == 3 ? t / n1 : 0;
+  uint32_t b = 0;
+  for (int l = 0; l < n1; ++l) {
+    const long long node = dim == 3 ? (long long)(ex * degree + i) +
+                                          (long long)lat.nodes[0] * ((long long)(ey * degree + j) +
+                                                                     (long long)lat.nodes[1] * (long long)(ez * degree + l))
+                                    : (long long)(ex * degree + i) + (long long)lat.nodes[0] * (long long)(ey * degree + l);
+    for (int c = 0; c < dim; ++c)
+      if (mask[node * dim + c]) b |= 1u << (c * n1 + l);
+  }
+  bits[id] = b;
 }
 
 }  // namespace hf

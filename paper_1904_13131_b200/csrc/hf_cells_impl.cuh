@@ -1,8 +1,54 @@
 // Instantiation/dispatch of the cell kernels for one dimension.
 #pragma once
 #include "hf_dispatch.h"
+#include "hf_line.cuh"
+
 
 namespace hf {
+
+// Launch of the line-parallel apply (hf_line.cuh): persistent warps, grid
+// sized to the resident capacity (148 SMs x blocks per SM) or the tile count.
+template <int DIM, int N, int VAR>
+cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
+  using K = LineCfg<DIM, N>;
+  using PL = LinePlan<DIM, N, VAR>;
+  static int resident = -1;
+  if (resident < 0) {
+    cudaError_t e = cudaFuncSetAttribute(k_apply_line<DIM, N, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)PL::SMEM);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, dev = 0, nsm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_line<DIM, N, VAR>, PL::NT, PL::SMEM);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    resident = (per_sm > 0 ? per_sm : 1) * (nsm > 0 ? nsm : 148);
+  }
+  LineArgs a;
+  a.lat = c.lat;
+  a.degree = c.degree;
+  a.x = c.x;
+  a.y = c.y;
+  a.cache = c.cache;
+  a.ubar = c.ubar;
+  a.mu = c.mu;
+  a.lam = c.lam;
+  a.mask = c.mask;
+  a.lmask = c.lmask;
+  a.skip = c.skip;
+  TabLine<N> T;
+  for (int l = 0; l < N; ++l)
+    for (int o = 0; o < N; ++o) {
+      T.V[l][o] = c.tab.V[l * N + o];
+      T.Dc[l][o] = c.tab.Dc[l * N + o];
+    }
+  const long long tiles = (c.lat.n_el + K::CPW - 1) / K::CPW;
+  long long nb = (tiles + PL::W - 1) / PL::W;
+  if (nb > resident) nb = resident;
+  if (nb <= 0) return cudaSuccess;
+  k_apply_line<DIM, N, VAR><<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);
+  return cudaGetLastError();
+}
 
 template <int DIM, int N>
 cudaError_t launch_one(int op, int var, const CellArgs& a, int mode, double target, unsigned long long* first,
@@ -14,10 +60,9 @@ cudaError_t launch_one(int op, int var, const CellArgs& a, int mode, double targ
   size_t sm = K::SMEM;
   switch (op) {
     case OP_APPLY:
-      if (var == SCALAR) k_apply<DIM, N, SCALAR><<<grid, block, sm, s>>>(a);
-      else if (var == TENSOR2) k_apply<DIM, N, TENSOR2><<<grid, block, sm, s>>>(a);
-      else k_apply<DIM, N, TENSOR4><<<grid, block, sm, s>>>(a);
-      break;
+      if (var == SCALAR) return launch_apply_line<DIM, N, SCALAR>(a, s);
+      if (var == TENSOR2) return launch_apply_line<DIM, N, TENSOR2>(a, s);
+      return launch_apply_line<DIM, N, TENSOR4>(a, s);
     case OP_BUILD:
       if (var == SCALAR) k_build<DIM, N, SCALAR><<<grid, block, sm, s>>>(a);
       else if (var == TENSOR2) k_build<DIM, N, TENSOR2><<<grid, block, sm, s>>>(a);

@@ -109,3 +109,40 @@ template <int NV>
 HF_DEV constexpr int hf_triu(int r, int c) {
   return r * NV - (r * (r - 1)) / 2 + (c - r);
 }
+
+// ---- warp-tile geometry of the line kernels and the tiled q-point cache ----
+// (hf_line.cuh).  A warp tile holds CPW whole cells; its cache block is
+// [field][iq][lane] with lane = cell_in_tile * L + line (x-lines).
+template <int DIM, int N>
+struct LineCfg {
+  static constexpr int NQ = (DIM == 2) ? N * N : N * N * N;
+  static constexpr int L = NQ / N;        // lines per cell
+  static constexpr int CPW = 32 / L;      // cells per warp tile
+  static constexpr int LANES = CPW * L;   // active lanes of a warp
+  static constexpr int TS = CPW * NQ;     // q-points per tile
+};
+
+// Tiled q-point cache: [tile][iq][field][lane], one contiguous "chunk" of
+// nf*LANES doubles (rounded to 16 bytes) per (tile, iq) -- the unit a TMA bulk
+// copy moves into shared memory (hf_line.cuh).
+template <int DIM, int N>
+struct TileLayout {
+  using K = LineCfg<DIM, N>;
+  HF_DEV static constexpr long long chunk(int nf) { return ((long long)nf * K::LANES + 1) & ~1ll; }
+  HF_DEV static constexpr long long stride(int nf) { return N * chunk(nf); }
+  // flat index of field f of (cell e, local q-point lq, x fastest)
+  HF_DEV static long long index(long long e, int lq, int f, int nf) {
+    const long long tile = e / K::CPW;
+    const int m = (int)(e - tile * K::CPW);
+    const int iq = lq % N, line = lq / N;
+    return tile * stride(nf) + iq * chunk(nf) + (long long)f * K::LANES + m * K::L + line;
+  }
+};
+inline long long tile_cache_doubles(int dim, int n1, int nf, long long n_el) {
+  int nq = dim == 2 ? n1 * n1 : n1 * n1 * n1;
+  int lanes = (32 / (nq / n1)) * (nq / n1);
+  int cpw = 32 / (nq / n1);
+  long long tiles = (n_el + cpw - 1) / cpw;
+  long long ch = ((long long)nf * lanes + 1) & ~1ll;
+  return tiles * n1 * ch;
+}

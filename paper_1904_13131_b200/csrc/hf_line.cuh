@@ -1,0 +1,543 @@
+// Line-parallel, TMA-fed apply kernel of the matrix-free Neo-Hookean tangent
+// (sm_100a, fp64).  DESIGN.md §4.1 has the measurements behind each choice.
+//
+//  * One thread owns one 1D LINE of a cell (N points along one axis). Every 1D
+//    contraction of the sum factorisation runs in registers with a warp-uniform
+//    table index. The tables are kernel parameters (constant-bank operands of
+//    DFMA), so no shared-memory table traffic.
+//  * A consumer warp holds CPW = 32 / N^(DIM-1) whole cells (a "warp tile").
+//    The only synchronisation between axis phases is __syncwarp. Lines are
+//    handed from one axis to the next through a per-warp shared-memory slice
+//    whose layout (cells interleaved, padded strides) is chosen per (DIM, N) to
+//    minimise bank conflicts of the 64-bit accesses.
+//  * The quadrature cache is stored per tile as [tile][iq][field][lane], so the
+//    data of one (tile, iq) is a contiguous chunk. Every warp streams its own
+//    chunks through a private ring of RW shared-memory stages with 1D TMA bulk
+//    copies (cp.async.bulk ... mbarrier::complete_tx): it issues chunk j+RW as
+//    soon as chunk j is consumed, and waits on a stage's mbarrier only right
+//    before the point phase. Private rings keep every wait at most one phase
+//    ahead of its barrier (a ring shared by several consumers lets a fast warp
+//    alias the parity of a slow one's stage).
+//    The HBM stream therefore never occupies registers: the bytes in flight are
+//    bounded by the rings, not by occupancy. The first kernel generation was
+//    latency bound at 16 warps/SM with the cache loaded into registers.
+//
+// Phases of one warp tile (3D; 2D drops axis 2):
+//   E1  z-lines : gather x (constrained DoFs zeroed), interpolate along z      -> A
+//   E2  y-lines : interpolate along y                                         A -> B
+//   E3  x-lines : interpolate along x (values Q at Gauss points), collocation
+//                 derivative along x kept in registers (Gx)                    B -> A(Q)
+//   E4  y-/z-lines : collocation derivatives along y and z                   A -> B(G1), C(G2)
+//   P   x-lines : q-point physics of the caching variant (operators.py:341-392)
+//                 from the TMA stage; queued G[c][a]*JxW written to A/B/C
+//   I1  a-lines : transposed collocation derivative along axis a (in place)
+//   I2  x-lines : sum of the three, transposed interpolation along x           A
+//   I3  y-lines : transposed interpolation along y                             A
+//   I4  z-lines : transposed interpolation along z + atomic scatter-add,
+//                 constrained rows dropped (fespace.py:307-324)
+//
+// Reference correspondence: gather fespace.py:291-293 + operators.py:333-334;
+// evaluate fespace.py:224-239; q-point physics operators.py:341-392; integrate
+// fespace.py:258-288; scatter fespace.py:296-324.
+#pragma once
+#include "hf_cell.cuh"
+
+namespace hf {
+
+// 1D tables as a kernel parameter: indexed with compile-time constants only,
+// so they are constant-bank operands.
+template <int N>
+struct TabLine {
+  double V[N][N];   // V[l][o]  = N_l(xi_o)
+  double Dc[N][N];  // Dc[l][o] = collocation derivative at Gauss point o of Gauss-basis l
+};
+
+struct LineArgs {
+  HfLattice lat;
+  int degree;
+  const double* x;
+  double* y;
+  const double* cache;  // tiled [tile][iq][field][lane]
+  const double* ubar;   // scalar strategy
+  const double* mu;     // scalar strategy
+  const double* lam;
+  const uint8_t* mask;
+  const uint32_t* lmask;  // constraint bits per (cell, last-axis line)
+  const int* skip;
+};
+
+// Per-warp line-buffer layout: element (cell m, component c, point i,j,k) at
+// ((c*NP + i + j*SJ + k*SK) * CPWP + m).  (CPWP, PJ, PK) from a bank-conflict
+// search over the 64-bit access patterns of every axis phase.
+template <int DIM, int N>
+struct LineLay {
+  static constexpr int CPWP = DIM == 3 ? (N == 2 ? 12 : (N == 5 ? 1 : 3))
+                                       : (N == 2 ? 18 : N == 3 ? 11 : N == 4 ? 12 : N == 5 ? 9 : N == 6 ? 5
+                                          : N == 7 ? 6 : N == 8 ? 6 : 9);
+  static constexpr int PJ = DIM == 3 ? (N == 4 ? 1 : 0) : (N == 2 || N == 9 ? 2 : (N == 3 || N == 4 || N == 8) ? 1 : 0);
+  static constexpr int PK = (DIM == 3 && N == 2) ? 2 : 0;
+  static constexpr int SJ = N + PJ;
+  static constexpr int SK = DIM == 3 ? N * SJ + PK : 0;
+  static constexpr int NP = DIM == 3 ? N * SK : N * SJ;  // points incl. padding
+  static constexpr int BUF = DIM * NP * CPWP;           // doubles per buffer per warp
+};
+
+template <int DIM, int N, int AX>
+HF_DEV constexpr int lstride() {
+  using Y = LineLay<DIM, N>;
+  return AX == 0 ? 1 : (AX == 1 ? Y::SJ : Y::SK);
+}
+// padded offset of point 0 of line t along axis AX
+template <int DIM, int N, int AX>
+HF_DEV int lbase(int t) {
+  using Y = LineLay<DIM, N>;
+  if (DIM == 2) return AX == 0 ? t * Y::SJ : t;
+  if (AX == 0) return (t % N) * Y::SJ + (t / N) * Y::SK;
+  if (AX == 1) return (t % N) + (t / N) * Y::SK;
+  return (t % N) + (t / N) * Y::SJ;
+}
+
+// out[o] = sum_l M[l][o] in[l]   (forward)      out[l] = sum_o M[l][o] in[o]   (transposed)
+template <int N, bool TR>
+HF_DEV void c1d(const double (&M)[N][N], const double* in, double* out) {
+#pragma unroll
+  for (int o = 0; o < N; ++o) {
+    double s = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) s = fma(TR ? M[o][l] : M[l][o], in[l], s);
+    out[o] = s;
+  }
+}
+
+template <int DIM, int N, int AX>
+HF_DEV void ld_line(const double* cell, int t, double (&v)[DIM][N]) {
+  using Y = LineLay<DIM, N>;
+  const int b = lbase<DIM, N, AX>(t);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c)
+#pragma unroll
+    for (int l = 0; l < N; ++l) v[c][l] = cell[(c * Y::NP + b + l * lstride<DIM, N, AX>()) * Y::CPWP];
+}
+template <int DIM, int N, int AX>
+HF_DEV void st_line(double* cell, int t, const double (&v)[DIM][N]) {
+  using Y = LineLay<DIM, N>;
+  const int b = lbase<DIM, N, AX>(t);
+#pragma unroll
+  for (int c = 0; c < DIM; ++c)
+#pragma unroll
+    for (int l = 0; l < N; ++l) cell[(c * Y::NP + b + l * lstride<DIM, N, AX>()) * Y::CPWP] = v[c][l];
+}
+template <int DIM, int N, bool TR>
+HF_DEV void c_line(const double (&M)[N][N], double (&v)[DIM][N]) {
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    double o[N];
+    c1d<N, TR>(M, v[c], o);
+#pragma unroll
+    for (int l = 0; l < N; ++l) v[c][l] = o[l];
+  }
+}
+
+// first lattice node of cell e
+template <int DIM>
+HF_DEV long long cell_node0(const HfLattice& lat, long long e, int degree) {
+  long long r = e;
+  const int ex = (int)(r % lat.cells[0]);
+  r /= lat.cells[0];
+  const int ey = (int)(r % lat.cells[1]);
+  const int ez = (DIM == 3) ? (int)(r / lat.cells[1]) : 0;
+  return (long long)ex * degree +
+         (long long)lat.nodes[0] * ((long long)ey * degree + (long long)lat.nodes[1] * ((long long)ez * degree));
+}
+
+// first node and stride (in nodes) of line t along the last axis
+template <int DIM, int N>
+HF_DEV void last_axis_line(const HfLattice& lat, long long node0, int t, long long& nb, long long& s_last) {
+  const int i = t % N;
+  const int j = DIM == 3 ? t / N : 0;
+  const long long sy = lat.nodes[0];
+  s_last = DIM == 3 ? sy * lat.nodes[1] : sy;
+  nb = node0 + i + (DIM == 3 ? j * sy : 0);
+}
+
+// The last-axis line of one tile gathered ahead of use (software pipelining
+// one tile deep): nodal values of x (and ubar for the scalar strategy) and the
+// line's constraint bits (bit c*N + l).
+template <int DIM, int N, int VAR>
+struct Gather {
+  double u[DIM][N];
+  double ub[DIM][N];  // scalar strategy only
+  unsigned mb;
+  long long e, node0;
+  bool live;
+};
+
+template <int DIM, int N, int VAR>
+HF_DEV void gather_tile(const LineArgs& a, long long tile, long long ntiles, int m, int t, bool act,
+                        Gather<DIM, N, VAR>& g) {
+  using K = LineCfg<DIM, N>;
+  g.e = tile * K::CPW + m;
+  g.live = act && tile < ntiles && g.e < a.lat.n_el;
+  g.mb = 0;
+  g.node0 = g.live ? cell_node0<DIM>(a.lat, g.e, a.degree) : 0;
+  if (!g.live) return;
+  long long nb, s_last;
+  last_axis_line<DIM, N>(a.lat, g.node0, t, nb, s_last);
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    const long long d0 = (nb + l * s_last) * DIM;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      g.u[c][l] = __ldg(a.x + d0 + c);
+      if (VAR == SCALAR) g.ub[c][l] = __ldg(a.ubar + d0 + c);
+    }
+  }
+  g.mb = __ldg(a.lmask + g.e * K::L + t);
+}
+
+// Unit-cell gradients of the nodal line values u0 (last axis, already masked)
+// of the warp's cells: Gx in registers
+// (x-line owners), the axis-1 derivative in buffer g1, axis-2 (3D) in g2.
+// Buffers a and b are scratch.
+template <int DIM, int N>
+HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live, int t, double* a, double* b,
+                      double* g1, double* g2, double (&Gx)[DIM][N]) {
+  double u[DIM][N];
+  if (live) {
+#pragma unroll
+    for (int c = 0; c < DIM; ++c)
+#pragma unroll
+      for (int l = 0; l < N; ++l) u[c][l] = u0[c][l];
+    c_line<DIM, N, false>(T.V, u);
+    st_line<DIM, N, DIM - 1>(DIM == 3 ? a : b, t, u);
+  }
+  __syncwarp();
+  if (DIM == 3) {
+    if (live) {
+      ld_line<DIM, N, 1>(a, t, u);
+      c_line<DIM, N, false>(T.V, u);
+      st_line<DIM, N, 1>(b, t, u);
+    }
+    __syncwarp();
+  }
+  if (live) {
+    ld_line<DIM, N, 0>(b, t, u);
+    c_line<DIM, N, false>(T.V, u);
+    st_line<DIM, N, 0>(a, t, u);  // Q at Gauss points
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) c1d<N, false>(T.Dc, u[c], Gx[c]);
+  }
+  __syncwarp();
+  if (live) {
+    ld_line<DIM, N, 1>(a, t, u);
+    c_line<DIM, N, false>(T.Dc, u);
+    st_line<DIM, N, 1>(g1, t, u);
+    if (DIM == 3) {
+      ld_line<DIM, N, DIM - 1>(a, t, u);
+      c_line<DIM, N, false>(T.Dc, u);
+      st_line<DIM, N, DIM - 1>(g2, t, u);
+    }
+  }
+  __syncwarp();
+}
+
+// ---- mbarrier / TMA bulk-copy primitives (PTX) ----
+HF_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+HF_DEV void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+HF_DEV bool mbar_try(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// wait for the phase of parity `parity`; a wait that cannot complete traps
+// after ~10 s instead of hanging the device
+HF_DEV void mbar_wait(unsigned long long* b, unsigned parity) {
+  if (mbar_try(b, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(b, parity))
+    if (clock64() - t0 > 20000000000ll) __trap();
+}
+HF_DEV void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+HF_DEV void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+HF_DEV void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// shared-memory plan of one block of W warps, each with NB line buffers and a
+// private ring of RW cache stages
+template <int DIM, int N, int VAR>
+struct LinePlan {
+  using K = LineCfg<DIM, N>;
+  static constexpr int NB = (VAR == SCALAR) ? 5 : 3;
+  static constexpr int NF = (VAR == SCALAR) ? 2 + DIM * DIM : CacheFields<DIM, VAR>::NF;
+  static constexpr long long CH = TileLayout<DIM, N>::chunk(NF);  // doubles per (tile, iq) chunk
+  static constexpr size_t BUDGET = 226 * 1024;
+  static constexpr size_t perw(int rw) {
+    return sizeof(double) * ((size_t)rw * CH + (size_t)NB * LineLay<DIM, N>::BUF) + 16 * rw;
+  }
+  // RW = min(N, 3) stages: at Q2 the chunks of the next tile are issued while
+  // the current tile's point phase consumes its own, one tile period ahead of
+  // use (RW = 2 < N stalled the point phase on the TMA barrier); at Q4 a full
+  // tile of stages would cost 3 of 7 resident warps, so the ring stays 3 deep.
+  static constexpr int RW = N < 3 ? N : 3;
+  static constexpr int W0 = (int)(BUDGET / perw(RW));
+  static constexpr int W = W0 > 8 ? 8 : (W0 < 1 ? 1 : W0);
+  static constexpr int NT = 32 * W;
+  static constexpr size_t SMEM = (size_t)W * perw(RW);
+};
+
+template <int DIM, int N, int VAR>
+__global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(const LineArgs a, const TabLine<N> T) {
+  using K = LineCfg<DIM, N>;
+  using PL = LinePlan<DIM, N, VAR>;
+  using Y = LineLay<DIM, N>;
+  constexpr int NF = PL::NF;
+  constexpr int NB = PL::NB;
+  constexpr int W = PL::W;
+  constexpr int RW = PL::RW;
+  constexpr long long CH = PL::CH;
+  constexpr int NV = DIM * (DIM + 1) / 2;
+  constexpr int NM = NV * (NV + 1) / 2;
+  if (a.skip && *a.skip) return;
+  extern __shared__ __align__(128) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ring = smem + (size_t)warp * RW * CH;  // this warp's stages (16-byte aligned)
+  double* lbuf = smem + (size_t)W * RW * CH;      // W x NB x BUF
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(lbuf + (size_t)W * NB * Y::BUF) + warp * RW;
+  const long long ntiles = (a.lat.n_el + K::CPW - 1) / K::CPW;
+  const long long tstride = (long long)N * CH;
+  // chunk j of this warp: tile blockIdx.x + (warp + (j / N) * W) * gridDim.x, iq = j % N
+  auto issue = [&](long long j) {
+    const long long tile = blockIdx.x + (warp + (j / N) * W) * (long long)gridDim.x;
+    if (tile >= ntiles) return;
+    const int s = (int)(j % RW);
+    mbar_expect_tx(full + s, (unsigned)(CH * sizeof(double)));
+    tma_load_1d(ring + (size_t)s * CH, a.cache + tile * tstride + (j % N) * CH, (unsigned)(CH * sizeof(double)),
+                full + s);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < RW; ++s) mbar_init(full + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int j = 0; j < RW; ++j) issue(j);
+  }
+  __syncwarp();
+
+  const int m = lane / K::L;
+  const int t = lane - m * K::L;
+  const bool act = lane < K::LANES;
+  double* wb = lbuf + (size_t)warp * NB * Y::BUF + (act ? m : 0);
+  double* bufs[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) bufs[b] = wb + b * Y::BUF;
+  double* Q = DIM == 3 ? bufs[0] : bufs[1];   // Q, later the x part of the queued data
+  double* Sc = DIM == 3 ? bufs[1] : bufs[0];  // scratch of the evaluation
+  double* G1 = DIM == 3 ? bufs[1] : bufs[0];
+  double* G2 = bufs[2];
+
+  long long jc = 0;  // this warp's chunk counter
+  const long long tstep = (long long)W * gridDim.x;
+  Gather<DIM, N, VAR> nxt;
+  gather_tile<DIM, N, VAR>(a, blockIdx.x + (long long)warp * gridDim.x, ntiles, m, t, act, nxt);
+  for (long long tile = blockIdx.x + (long long)warp * gridDim.x; tile < ntiles; tile += tstep) {
+    const Gather<DIM, N, VAR> g = nxt;
+    gather_tile<DIM, N, VAR>(a, tile + tstep, ntiles, m, t, act, nxt);  // in flight during this tile
+    const long long e = g.e;
+    const bool live = g.live;
+    double u[DIM][N];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c)
+#pragma unroll
+      for (int l = 0; l < N; ++l) u[c][l] = ((g.mb >> (c * N + l)) & 1u) ? 0.0 : g.u[c][l];
+
+    double Gx[DIM][N];
+    double Gxu[DIM][N];  // scalar: x part of the gradient of ubar
+    if (VAR == SCALAR) eval_line<DIM, N>(T, g.ub, live, t, Q, Sc, bufs[3], bufs[4], Gxu);
+    eval_line<DIM, N>(T, u, live, t, Q, Sc, G1, G2, Gx);
+
+    // ---------------- P: q-point physics along this thread's x-line ----------------
+    double mu = 0.0, lam = 0.0;
+    if (VAR == SCALAR && live) {
+      mu = __ldg(a.mu + e);
+      lam = __ldg(a.lam + e);
+    }
+    const int pt0 = lbase<DIM, N, 0>(t);
+#pragma unroll
+    for (int iq = 0; iq < N; ++iq, ++jc) {
+      const int s = (int)(jc % RW);
+      mbar_wait(full + s, (unsigned)((jc / RW) & 1));
+      const double* st = ring + (size_t)s * CH + lane;
+      if (live) {
+        const int pt = pt0 + iq;
+        double f[NF];
+#pragma unroll
+        for (int q = 0; q < NF; ++q) f[q] = st[q * K::LANES];
+        double gu[DIM][DIM];
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc) {
+          gu[cc][0] = Gx[cc][iq];
+          gu[cc][1] = G1[(cc * Y::NP + pt) * Y::CPWP];
+          if (DIM == 3) gu[cc][DIM - 1] = G2[(cc * Y::NP + pt) * Y::CPWP];
+        }
+        double G[DIM][DIM];
+        if (VAR == TENSOR4) {
+          double sinv[DIM][DIM], tau[DIM][DIM];
+#pragma unroll
+          for (int i = 0; i < DIM; ++i)
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+              tau[i][j] = f[hf_slot<DIM>(i, j)];
+              sinv[i][j] = f[NV + NM + i * DIM + j];
+            }
+          qp_action<DIM, true>(gu, sinv, tau, 0.0, 0.0, f + NV, f[NF - 1], G);
+        } else if (VAR == TENSOR2) {
+          double sinv[DIM][DIM], tau[DIM][DIM];
+#pragma unroll
+          for (int i = 0; i < DIM; ++i)
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+              tau[i][j] = f[2 + hf_slot<DIM>(i, j)];
+              sinv[i][j] = f[2 + NV + i * DIM + j];
+            }
+          qp_action<DIM, false>(gu, sinv, tau, f[0], f[1], nullptr, f[NF - 1], G);
+        } else {
+          // rebuild F, b, tau = mu b - c1 I and s_inv from ubar (operators.py:349-363)
+          double ji[DIM][DIM];
+#pragma unroll
+          for (int r = 0; r < DIM; ++r)
+#pragma unroll
+            for (int q = 0; q < DIM; ++q) ji[r][q] = f[1 + r * DIM + q];
+          double gub[DIM][DIM];
+#pragma unroll
+          for (int cc = 0; cc < DIM; ++cc) {
+            gub[cc][0] = Gxu[cc][iq];
+            gub[cc][1] = bufs[3][(cc * Y::NP + pt) * Y::CPWP];
+            if (DIM == 3) gub[cc][DIM - 1] = bufs[4][(cc * Y::NP + pt) * Y::CPWP];
+          }
+          double F[DIM * DIM];
+#pragma unroll
+          for (int i = 0; i < DIM; ++i)
+#pragma unroll
+            for (int Aa = 0; Aa < DIM; ++Aa) {
+              double sm = (i == Aa) ? 1.0 : 0.0;
+#pragma unroll
+              for (int q = 0; q < DIM; ++q) sm = fma(gub[i][q], ji[q][Aa], sm);
+              F[i * DIM + Aa] = sm;
+            }
+          const double c1 = f[0];
+          double tau[DIM][DIM], sinv[DIM][DIM], Fi[DIM * DIM];
+#pragma unroll
+          for (int i = 0; i < DIM; ++i)
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+              double bb = 0.0;
+#pragma unroll
+              for (int Aa = 0; Aa < DIM; ++Aa) bb = fma(F[i * DIM + Aa], F[j * DIM + Aa], bb);
+              tau[i][j] = mu * bb - (i == j ? c1 : 0.0);
+            }
+          hf_inv<DIM>(F, hf_det<DIM>(F), Fi);
+#pragma unroll
+          for (int q = 0; q < DIM; ++q)
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) {
+              double sm = 0.0;
+#pragma unroll
+              for (int Aa = 0; Aa < DIM; ++Aa) sm = fma(ji[q][Aa], Fi[Aa * DIM + j], sm);
+              sinv[q][j] = sm;
+            }
+          qp_action<DIM, false>(gu, sinv, tau, 2.0 * c1, 2.0 * lam, nullptr, f[NF - 1], G);
+        }
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc) {
+          Q[(cc * Y::NP + pt) * Y::CPWP] = G[cc][0];
+          G1[(cc * Y::NP + pt) * Y::CPWP] = G[cc][1];
+          if (DIM == 3) G2[(cc * Y::NP + pt) * Y::CPWP] = G[cc][DIM - 1];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {  // stage consumed by every lane: refill it with chunk jc + RW
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(jc + RW);
+      }
+    }
+    __syncwarp();
+    // ---------------- I1: transposed collocation derivative per axis, in place ----------------
+    if (live) {
+      double v[DIM][N];
+      ld_line<DIM, N, 0>(Q, t, v);
+      c_line<DIM, N, true>(T.Dc, v);
+      st_line<DIM, N, 0>(Q, t, v);
+      ld_line<DIM, N, 1>(G1, t, v);
+      c_line<DIM, N, true>(T.Dc, v);
+      st_line<DIM, N, 1>(G1, t, v);
+      if (DIM == 3) {
+        ld_line<DIM, N, DIM - 1>(G2, t, v);
+        c_line<DIM, N, true>(T.Dc, v);
+        st_line<DIM, N, DIM - 1>(G2, t, v);
+      }
+    }
+    __syncwarp();
+    // ---------------- I2: sum, transposed interpolation along x ----------------
+    if (live) {
+      double v[DIM][N], w[DIM][N];
+      ld_line<DIM, N, 0>(Q, t, v);
+      ld_line<DIM, N, 0>(G1, t, w);
+#pragma unroll
+      for (int cc = 0; cc < DIM; ++cc)
+#pragma unroll
+        for (int l = 0; l < N; ++l) v[cc][l] += w[cc][l];
+      if (DIM == 3) {
+        ld_line<DIM, N, 0>(G2, t, w);
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc)
+#pragma unroll
+          for (int l = 0; l < N; ++l) v[cc][l] += w[cc][l];
+      }
+      c_line<DIM, N, true>(T.V, v);
+      st_line<DIM, N, 0>(Q, t, v);
+    }
+    __syncwarp();
+    if (DIM == 3) {
+      if (live) {
+        double v[DIM][N];
+        ld_line<DIM, N, 1>(Q, t, v);
+        c_line<DIM, N, true>(T.V, v);
+        st_line<DIM, N, 1>(Q, t, v);
+      }
+      __syncwarp();
+    }
+    // ---------------- I4: last axis, scatter-add ----------------
+    if (live) {
+      double v[DIM][N];
+      ld_line<DIM, N, DIM - 1>(Q, t, v);
+      c_line<DIM, N, true>(T.V, v);
+      long long nb, s_last;
+      last_axis_line<DIM, N>(a.lat, g.node0, t, nb, s_last);
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        const long long d0 = (nb + l * s_last) * DIM;
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc)
+          if (!((g.mb >> (cc * N + l)) & 1u)) atomicAdd(a.y + d0 + cc, v[cc][l]);
+      }
+    }
+    __syncwarp();  // line buffers are reused by the next tile
+  }
+}
+
+}  // namespace hf
