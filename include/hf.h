@@ -160,6 +160,10 @@ HF_API int hf_cg_update_p(long long n, double* p, const double* z, const double*
 /* z = inv_d r; out_dev[0] = r . z */
 HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, const double* inv_d, double* out_dev,
                          void* stream);
+/* reverse halo add of a slab interface (multi-GPU; no reference
+ * analogue -- the paper's MPI ghost exchange):
+ * y[i] += recv[i] where mask[i] == 0 */
+HF_API int hf_halo_add(long long n, double* y, const double* recv, const unsigned char* mask, void* stream);
 /* y = a x + b y */
 HF_API int hf_axpby(long long n, double a, const double* x, double b, double* y, void* stream);
 

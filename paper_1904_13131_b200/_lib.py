@@ -68,6 +68,7 @@ _SIGS = {
     "hf_cg_update_p": (I, [LL, P, P, P, I, I, P]),
     "hf_jacobi_dot": (I, [P, LL, P, P, P, P, P]),
     "hf_axpby": (I, [LL, D, P, D, P, P]),
+    "hf_halo_add": (I, [LL, P, P, P, P]),
 }
 
 

@@ -620,6 +620,14 @@ HF_API int hf_fill_masked(long long n, double* y, const double* x, const unsigne
   return HF_OK;
 }
 
+HF_API int hf_halo_add(long long n, double* y, const double* recv, const unsigned char* mask, void* stream) {
+  if (!y || !recv || !mask) return fail(HF_ERR_ARG, "null argument");
+  if (n <= 0) return HF_OK;
+  k_halo_add<<<vec_blocks(n), 256, 0, S(stream)>>>(n, y, recv, mask);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
 HF_API int hf_cheb_step(long long n, double* x, double* d, const double* b, const double* ax, const double* inv_d,
                         int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
                         void* stream) {

@@ -48,6 +48,14 @@ HF_DEV void grid_reduce(double v, double* partials, unsigned* counter, double* o
   }
 }
 
+// reverse halo add of a multi-GPU slab interface: y[i] += recv[i] on the
+// unconstrained DoFs (constrained ones hold the identity value on both ranks)
+__global__ void k_halo_add(long long n, double* __restrict__ y, const double* __restrict__ recv,
+                           const unsigned char* __restrict__ mask) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (!mask[i]) y[i] += recv[i];
+}
+
 inline unsigned red_blocks(long long n) {
   long long b = (n + RED_THREADS * 4 - 1) / (RED_THREADS * 4);
   if (b < 1) b = 1;

@@ -1,0 +1,558 @@
+"""Multi-GPU slab decomposition of the matrix-free tangent, GMG and CG.
+
+The reference is single-process; the paper partitioned cells
+over MPI ranks.  Here one process drives one GPU:
+
+* **Partition.**  Cells are cut into contiguous slabs along the last axis (z in
+  3D, y in 2D), one slab per rank, nested across GMG levels (a rank's coarse
+  slab is its fine slab halved).  With x fastest and the last axis slowest in
+  the reference numbering (fespace.py:3-8), a slab's lattice nodes are a
+  CONTIGUOUS range of global DoFs: the local vector of a rank is the slice
+  ``global[offset : offset + n_local]``.  Neighbouring slabs share one node
+  plane (the interface), which both ranks store.
+* **Consistency.**  Every distributed vector keeps identical values in both
+  copies of an interface plane.  Inputs of the operator are therefore
+  complete; one exchange per application suffices: the reverse add of the
+  partial sums on the interface plane (``SlabExchange.add``, NCCL send/recv,
+  then ``hf_halo_add``).  Constrained rows hold the identity value on both
+  ranks and are not added.
+* **Dots.**  Summed over the OWNED DoFs (a rank does not own its lower
+  interface plane), then all-reduced.
+* **Coarse levels.**  Levels whose slabs would be thinner than ``min_cells``
+  cells are replicated on every rank.  The restricted residual enters them
+  through an all-reduce of the zero-padded partial sums; every rank runs the
+  replicated V-cycle (the single-GPU ``GMGPreconditioner``, graph-captured) and
+  prolongates from its own slice.
+
+``Comm`` abstracts the transport: ``TorchComm`` over ``torch.distributed``
+(NCCL on the GPU box; gloo stages through host memory, used to run several
+ranks on one GPU in the tests), ``LocalComm`` for one rank.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device as dv
+from ._lib import check, lib
+from .fespace import ConstraintSet
+from .material import NonPositiveJacobian
+from .mesh import Mesh, sub_box
+from .multigrid import (ChebyshevSettings, GMGPreconditioner, TransferOperator, _cheb_coeffs, build_level_operators,
+                        build_transfers)
+from .operators import Material, MatrixFreeTangent, Problem, compute_residual
+
+
+# ---------------------------------------------------------------------------
+# transport
+# ---------------------------------------------------------------------------
+
+
+class LocalComm:
+    """One rank: every collective is the identity."""
+
+    rank, size = 0, 1
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        return t
+
+    def exchange(self, sends: dict, recvs: dict) -> None:
+        if sends or recvs:
+            raise ValueError("a single rank has no neighbours")
+
+    def barrier(self) -> None:
+        pass
+
+
+class TorchComm:
+    """torch.distributed transport (nccl: device buffers; gloo: staged through host)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        self.staged = dist.get_backend(group) != "nccl"
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.staged and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def exchange(self, sends: dict, recvs: dict) -> None:
+        """Point-to-point swap: ``sends[peer]`` -> peer, ``recvs[peer]`` <- peer."""
+        dist = self.dist
+        if self.staged:
+            s_h = {p: t.cpu() for p, t in sends.items()}
+            r_h = {p: torch.empty(t.shape, dtype=t.dtype) for p, t in recvs.items()}
+            ops = [dist.P2POp(dist.isend, s_h[p], p, self.group) for p in sorted(s_h)]
+            ops += [dist.P2POp(dist.irecv, r_h[p], p, self.group) for p in sorted(r_h)]
+            for w in dist.batch_isend_irecv(ops) if ops else []:
+                w.wait()
+            for p, t in recvs.items():
+                t.copy_(r_h[p])
+            return
+        ops = [dist.P2POp(dist.isend, sends[p], p, self.group) for p in sorted(sends)]
+        ops += [dist.P2POp(dist.irecv, recvs[p], p, self.group) for p in sorted(recvs)]
+        for w in dist.batch_isend_irecv(ops) if ops else []:
+            w.wait()
+
+    def barrier(self) -> None:
+        self.dist.barrier(group=self.group)
+
+
+# ---------------------------------------------------------------------------
+# partition
+# ---------------------------------------------------------------------------
+
+
+def slab_ranges(n_cells: int, size: int) -> list[tuple[int, int]]:
+    """Balanced contiguous cell ranges along the slab axis, one per rank."""
+    if size < 1 or n_cells < size:
+        raise ValueError(f"cannot cut {n_cells} cell layers into {size} slabs")
+    base, extra = divmod(n_cells, size)
+    out, c = [], 0
+    for r in range(size):
+        n = base + (1 if r < extra else 0)
+        out.append((c, c + n))
+        c += n
+    return out
+
+
+@dataclass(frozen=True)
+class Slab:
+    """One rank's box of a level: cells [c0, c1) along the last axis."""
+
+    dim: int
+    degree: int
+    cells: tuple  # global cells per axis
+    c0: int
+    c1: int
+
+    @property
+    def axis(self) -> int:
+        return self.dim - 1
+
+    @property
+    def plane_nodes(self) -> int:
+        return int(np.prod([c * self.degree + 1 for c in self.cells[:-1]]))
+
+    @property
+    def plane_dofs(self) -> int:
+        return self.plane_nodes * self.dim
+
+    @property
+    def n_global_dofs(self) -> int:
+        return self.plane_dofs * (self.cells[-1] * self.degree + 1)
+
+    @property
+    def dof_offset(self) -> int:
+        """First global DoF of the slab (its lower node plane)."""
+        return self.c0 * self.degree * self.plane_dofs
+
+    @property
+    def n_dofs(self) -> int:
+        return ((self.c1 - self.c0) * self.degree + 1) * self.plane_dofs
+
+    @property
+    def has_lower(self) -> bool:
+        return self.c0 > 0
+
+    @property
+    def has_upper(self) -> bool:
+        return self.c1 < self.cells[-1]
+
+    @property
+    def owned(self) -> slice:
+        """Local DoFs this rank owns (the lower interface plane belongs to the rank below)."""
+        return slice(self.plane_dofs if self.has_lower else 0, self.n_dofs)
+
+    def local(self, v_global):
+        return v_global[self.dof_offset:self.dof_offset + self.n_dofs]
+
+    def halved(self) -> "Slab":
+        if self.c0 % 2 or self.c1 % 2 or any(c % 2 for c in self.cells):
+            raise ValueError("slab does not coarsen 2:1")
+        return Slab(self.dim, self.degree, tuple(c // 2 for c in self.cells), self.c0 // 2, self.c1 // 2)
+
+
+def level_slabs(dim: int, degree: int, fine_cells: tuple, n_levels: int, rank: int, size: int,
+                min_cells: int = 2) -> list:
+    """Slabs of rank ``rank`` on every level, coarsest first.  A level is
+    distributed while every rank's slab keeps >= ``min_cells`` cell layers and
+    the slabs nest 2:1; the levels below, and always the coarsest, are
+    replicated (None)."""
+    ranges = slab_ranges(fine_cells[-1], size)
+    if min(b - a for a, b in ranges) < min(min_cells, fine_cells[-1] // size):
+        raise ValueError("the finest level is too thin to partition")
+    cells = tuple(fine_cells)
+    out = [Slab(dim, degree, cells, *ranges[rank])]
+    for _ in range(n_levels - 2):
+        ok = out[0] is not None and all(a % 2 == 0 and b % 2 == 0 for a, b in ranges) and \
+            all(c % 2 == 0 for c in cells) and min(b - a for a, b in ranges) // 2 >= min_cells
+        if ok:
+            ranges = [(a // 2, b // 2) for a, b in ranges]
+            cells = tuple(c // 2 for c in cells)
+            out.insert(0, out[0].halved())
+        else:
+            out.insert(0, None)
+    if n_levels > 1:
+        out.insert(0, None)  # the coarsest level is always replicated
+    return out
+
+
+# ---------------------------------------------------------------------------
+# distributed level objects
+# ---------------------------------------------------------------------------
+
+
+def _halo_add_dev(y: torch.Tensor, recv: torch.Tensor, mask: torch.Tensor) -> None:
+    check(lib().hf_halo_add(y.numel(), dv.ptr(y), dv.ptr(recv), dv.ptr(mask), dv.stream()))
+
+
+class SlabExchange:
+    """Reverse add of the interface-plane partial sums (the one exchange per apply).
+
+    ``add_fn(y_plane, recv, mask_plane)`` performs y += recv on unconstrained
+    entries; the product uses the libhf kernel (tests on CPU inject their own)."""
+
+    def __init__(self, slab: Slab, comm, mask_dev: torch.Tensor, add_fn=_halo_add_dev):
+        self.slab, self.comm, self.add_fn = slab, comm, add_fn
+        pd = slab.plane_dofs
+        self.pd = pd
+        self.peers = {}
+        if slab.has_lower:
+            self.peers[comm.rank - 1] = slice(0, pd)
+        if slab.has_upper:
+            self.peers[comm.rank + 1] = slice(slab.n_dofs - pd, slab.n_dofs)
+        self.recv = {p: torch.empty(pd, dtype=torch.float64, device=mask_dev.device) for p in self.peers}
+        self.mask = {p: mask_dev[s] for p, s in self.peers.items()}
+
+    def add(self, y: torch.Tensor) -> torch.Tensor:
+        if not self.peers:
+            return y
+        sends = {p: y[s].contiguous() for p, s in self.peers.items()}
+        self.comm.exchange(sends, self.recv)
+        for p, s in self.peers.items():
+            self.add_fn(y[s], self.recv[p], self.mask[p])
+        return y
+
+
+class DistProblem:
+    """A rank's slab of one level: the local ``Problem`` plus its partition data."""
+
+    def __init__(self, global_mesh: Mesh, degree: int, mat: Material, slab: Slab, comm, global_mask: np.ndarray,
+                 basis_nodes: str = "equispaced"):
+        self.slab, self.comm = slab, comm
+        self.global_mesh = global_mesh
+        local_mesh = sub_box(global_mesh, slab.axis, slab.c0, slab.c1)
+        self.local = Problem(local_mesh, degree, mat, basis_nodes=basis_nodes, has_top_face=not slab.has_upper)
+        mask = np.ascontiguousarray(slab.local(global_mask))
+        self.local.constraints = ConstraintSet.from_dofs(self.local.n_dofs, np.flatnonzero(mask))
+        self.mask_dev = torch.from_numpy(mask.astype(np.uint8)).cuda()
+        self.exchange = SlabExchange(slab, comm, self.mask_dev)
+
+    @property
+    def n_dofs(self) -> int:
+        return self.local.n_dofs
+
+    @property
+    def n_global_dofs(self) -> int:
+        return self.slab.n_global_dofs
+
+    def dot(self, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        """Global dot product: owned DoFs on this rank, all-reduced (2 scalars max per call site)."""
+        o = self.slab.owned
+        dv.dot(a[o], b[o], out)
+        return self.comm.allreduce_(out)
+
+    def residual(self, u: torch.Tensor, traction=None) -> torch.Tensor:
+        """compute_residual (operators.py:205-224) on the slab + interface add."""
+        return self.exchange.add(compute_residual(self.local, u, traction))
+
+
+def _agree_jacobian(comm, exc: NonPositiveJacobian | None, level=None):
+    """NonPositiveJacobian on any rank is raised on every rank."""
+    flag = torch.tensor([1.0 if exc is not None else 0.0], dtype=torch.float64, device="cuda")
+    comm.allreduce_(flag)
+    if exc is not None:
+        raise exc
+    if flag.item() > 0:
+        raise NonPositiveJacobian("det F <= 0 on another rank", element=-1, level=level)
+
+
+class DistributedTangent:
+    """MatrixFreeTangent on a slab: local cell kernel + reverse interface add."""
+
+    def __init__(self, dp: DistProblem, u_local, strategy: str = "tensor4", level=None):
+        self.dp = dp
+        err = None
+        try:
+            self.local = MatrixFreeTangent(dp.local, u_local, strategy)
+        except NonPositiveJacobian as e:
+            err = e
+        _agree_jacobian(dp.comm, err, level)
+        self.strategy = strategy
+
+    @property
+    def n_dofs(self) -> int:
+        return self.dp.n_dofs
+
+    def apply_into(self, x: torch.Tensor, y: torch.Tensor, skip=None) -> torch.Tensor:
+        self.local.apply_into(x, y, skip)
+        return self.dp.exchange.add(y)
+
+    def apply(self, x: torch.Tensor) -> torch.Tensor:
+        y = torch.empty_like(x)
+        return self.apply_into(x, y)
+
+    __call__ = apply
+
+    def diagonal(self) -> torch.Tensor:
+        return self.dp.exchange.add(self.local.diagonal())
+
+
+def dist_cg(dp: DistProblem, apply_fn, b: torch.Tensor, rel_tol: float = 1e-6, preconditioner=None,
+            max_iterations: int | None = None):
+    """PCG (solver.py:34-76) on slab vectors: local updates, all-reduced owned dots.
+    Returns (x, iterations, relative residual, residual history)."""
+    n = b.numel()
+    if max_iterations is None:
+        max_iterations = 10 * dp.n_global_dofs
+    L = lib()
+    s = torch.zeros(4, dtype=torch.float64, device="cuda")
+    x = torch.zeros_like(b)
+    r = b.clone()
+    ap = torch.empty_like(b)
+    dp.dot(b, b, s[0:1])
+    b_norm = float(np.sqrt(s[0].item()))
+    history = [b_norm]
+    if b_norm == 0.0:
+        return x, 0, 0.0, history
+    z = torch.empty_like(b)
+    if preconditioner is not None:
+        preconditioner.apply_into(r, z)
+    else:
+        z.copy_(r)
+    p = z.clone()
+    dp.dot(r, z, s[1:2])
+    rz = s[1].item()
+    from .solver import IndefiniteOperator
+
+    for it in range(1, max_iterations + 1):
+        apply_fn.apply_into(p, ap)
+        dp.dot(p, ap, s[2:3])
+        pap = s[2].item()
+        if pap <= 0.0:
+            raise IndefiniteOperator(f"p.Ap = {pap:.3e} <= 0 at iteration {it - 1}")
+        alpha = rz / pap
+        check(L.hf_axpby(n, alpha, dv.ptr(p), 1.0, dv.ptr(x), dv.stream()))
+        check(L.hf_axpby(n, -alpha, dv.ptr(ap), 1.0, dv.ptr(r), dv.stream()))
+        dp.dot(r, r, s[3:4])
+        r_norm = float(np.sqrt(s[3].item()))
+        history.append(r_norm)
+        if r_norm <= rel_tol * b_norm:
+            return x, it, r_norm / b_norm, history
+        if preconditioner is not None:
+            preconditioner.apply_into(r, z)
+        else:
+            z.copy_(r)
+        dp.dot(r, z, s[1:2])
+        rz_new = s[1].item()
+        check(L.hf_axpby(n, 1.0, dv.ptr(z), rz_new / rz, dv.ptr(p), dv.stream()))
+        rz = rz_new
+    return x, max_iterations, history[-1] / b_norm, history
+
+
+def dist_eigen_range(dp: DistProblem, op, diag: torch.Tensor, seed: int, iterations: int = 30):
+    """estimate_eigenvalue_range (multigrid.py:112-166) with all-reduced dots;
+    the Lanczos RHS is the rank's slice of the reference's global vector."""
+    import scipy.linalg
+
+    bg = np.random.default_rng(seed).standard_normal(dp.n_global_dofs)
+    b = torch.from_numpy(np.ascontiguousarray(dp.slab.local(bg))).cuda()
+    b[dp.mask_dev.bool()] = 0.0
+    n = b.numel()
+    L = lib()
+    inv_d = torch.reciprocal(diag)
+    s = torch.zeros(3, dtype=torch.float64, device="cuda")
+    r = b.clone()
+    z = inv_d * r
+    p = z.clone()
+    ap = torch.empty_like(r)
+    dp.dot(r, z, s[0:1])
+    rz = s[0].item()
+    alphas, betas = [], []
+    for _ in range(iterations):
+        if rz <= 0.0 or not np.isfinite(rz):
+            break
+        op.apply_into(p, ap)
+        dp.dot(p, ap, s[1:2])
+        pap = s[1].item()
+        if pap <= 0.0:
+            break
+        alpha = rz / pap
+        check(L.hf_axpby(n, -alpha, dv.ptr(ap), 1.0, dv.ptr(r), dv.stream()))
+        torch.mul(inv_d, r, out=z)
+        dp.dot(r, z, s[2:3])
+        rz_new = s[2].item()
+        if rz_new <= 1e-28 * rz or not np.isfinite(rz_new):
+            alphas.append(alpha)
+            break
+        beta = rz_new / rz
+        alphas.append(alpha)
+        betas.append(beta)
+        check(L.hf_axpby(n, 1.0, dv.ptr(z), beta, dv.ptr(p), dv.stream()))
+        rz = rz_new
+    if not alphas:
+        return 1.0, 1.0
+    k = len(alphas)
+    dt = np.empty(k)
+    dt[0] = 1.0 / alphas[0]
+    for i in range(1, k):
+        dt[i] = 1.0 / alphas[i] + betas[i - 1] / alphas[i - 1]
+    if k == 1:
+        return float(dt[0]), float(dt[0])
+    off = np.array([np.sqrt(betas[i]) / alphas[i] for i in range(k - 1)])
+    ritz = scipy.linalg.eigvalsh_tridiagonal(dt, off)
+    return float(ritz[0]), float(ritz[-1])
+
+
+class DistLevel:
+    """LevelOperator (multigrid.py:208-252) of a distributed level."""
+
+    def __init__(self, dp: DistProblem, u_local, strategy: str, seed: int, level: int):
+        self.dp, self.level = dp, level
+        self.op = DistributedTangent(dp, u_local, strategy, level=level)
+        self.diag = self.op.diagonal()
+        self.inv_diag = torch.reciprocal(self.diag)
+        self.lam_min, self.lam_max = dist_eigen_range(dp, self.op, self.diag, seed)
+        n = dp.n_dofs
+        self.b = torch.zeros(n, dtype=torch.float64, device="cuda")
+        self.x = torch.zeros_like(self.b)
+        self.d = torch.zeros_like(self.b)
+        self.ax = torch.zeros_like(self.b)
+        self.r = torch.zeros_like(self.b)
+
+    def smooth_into(self, b, x, steps: int, s: ChebyshevSettings, x_zero: bool):
+        theta, coefs = _cheb_coeffs(self.lam_max, s)
+        n, L = x.numel(), lib()
+        for step in range(steps):
+            zero = x_zero and step == 0
+            if not zero:
+                self.op.apply_into(x, self.ax)
+            check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(self.d), dv.ptr(b), None if zero else dv.ptr(self.ax),
+                                 dv.ptr(self.inv_diag), 1, theta, 0.0, 0.0, int(zero), None, dv.stream()))
+            for cd, cz in coefs:
+                self.op.apply_into(x, self.ax)
+                check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(self.d), dv.ptr(b), dv.ptr(self.ax), dv.ptr(self.inv_diag),
+                                     0, 0.0, cd, cz, 0, None, dv.stream()))
+        return x
+
+
+class DistGMG:
+    """V-cycle preconditioner (multigrid.py:309-351) over slab levels on top of
+    replicated coarse levels."""
+
+    def __init__(self, dist_levels: list, transfers: list, bridge: TransferOperator | None,
+                 replicated: GMGPreconditioner | None, coarse_slab: Slab | None, comm,
+                 smoothing_steps: int = 2, settings: ChebyshevSettings = ChebyshevSettings()):
+        self.levels, self.transfers = dist_levels, transfers
+        self.bridge, self.rep, self.cslab, self.comm = bridge, replicated, coarse_slab, comm
+        self.steps, self.settings = smoothing_steps, settings
+        if replicated is not None:
+            n = coarse_slab.n_global_dofs
+            self._cfull = torch.zeros(n, dtype=torch.float64, device="cuda")
+            self._xfull = torch.zeros(n, dtype=torch.float64, device="cuda")
+            self._cpart = torch.zeros(coarse_slab.n_dofs, dtype=torch.float64, device="cuda")
+
+    def _vc(self, i: int, b: torch.Tensor, x: torch.Tensor):
+        Lv = self.levels[i]
+        Lv.smooth_into(b, x, self.steps, self.settings, x_zero=True)
+        Lv.op.apply_into(x, Lv.ax)
+        n = b.numel()
+        check(lib().hf_resid_masked(n, dv.ptr(Lv.r), dv.ptr(b), dv.ptr(Lv.ax), dv.ptr(Lv.dp.mask_dev), dv.stream()))
+        if Lv.dp.slab.has_lower:  # the rank below owns the shared plane: count it once
+            Lv.r[:Lv.dp.slab.plane_dofs] = 0.0
+        if i == 0:
+            cs = self.cslab
+            self.bridge.restrict_into(Lv.r, self._cpart, mode=1)
+            self._cfull.zero_()
+            self._cfull[cs.dof_offset:cs.dof_offset + cs.n_dofs] = self._cpart
+            self.comm.allreduce_(self._cfull)
+            self.rep.apply_into(self._cfull, self._xfull)
+            self.bridge.prolong_into(self._xfull[cs.dof_offset:cs.dof_offset + cs.n_dofs], x, mode=2)
+        else:
+            C = self.levels[i - 1]
+            self.transfers[i - 1].restrict_into(Lv.r, C.b, mode=1)
+            C.dp.exchange.add(C.b)
+            self._vc(i - 1, C.b, C.x)
+            self.transfers[i - 1].prolong_into(C.x, x, mode=2)
+        Lv.smooth_into(b, x, self.steps, self.settings, x_zero=False)
+        return x
+
+    def apply_into(self, b: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        top = len(self.levels) - 1
+        out.zero_()
+        return self._vc(top, b, out)
+
+
+def build_dist_gmg(global_meshes: list, degree: int, mat: Material, global_masks: list, u_fine_local, comm,
+                   strategy: str = "tensor4", seed: int = 0, min_cells: int = 2):
+    """Distributed analogue of build_gmg (multigrid.py:372-382).
+
+    ``global_meshes``/``global_masks``: every level, coarsest first.  Returns
+    (DistGMG, fine DistProblem, fine DistributedTangent)."""
+    nlev = len(global_meshes)
+    fine = global_meshes[-1]
+    slabs = level_slabs(fine.dim, degree, fine.cells, nlev, comm.rank, comm.size, min_cells)
+    first = next(i for i, s in enumerate(slabs) if s is not None)
+    if first == 0:
+        raise ValueError("the coarsest level must be replicated (min_cells too small for the hierarchy)")
+    dps = {i: DistProblem(global_meshes[i], degree, mat, slabs[i], comm, global_masks[i])
+           for i in range(first, nlev)}
+    # injection of the fine state down the distributed levels (multigrid.py:76-92)
+    u = {nlev - 1: dv.as_dev(u_fine_local)}
+    for lvl in range(nlev - 1, first, -1):
+        uc = torch.empty(dps[lvl - 1].n_dofs, dtype=torch.float64, device="cuda")
+        check(lib().hf_inject(dps[lvl - 1].local._space, dps[lvl].local._space, dv.ptr(u[lvl]), dv.ptr(uc), 0,
+                              dv.stream()))
+        u[lvl - 1] = uc
+    levels = [DistLevel(dps[i], u[i], strategy, seed + 7919 * i, i) for i in range(first, nlev)]
+    transfers = [TransferOperator(dps[i].local, dps[i + 1].local) for i in range(first, nlev - 1)]
+    # replicated coarse levels: full coarse problems on every rank
+    rep_probs = []
+    for i in range(first):
+        p = Problem(global_meshes[i], degree, mat)
+        p.constraints = ConstraintSet.from_dofs(p.n_dofs, np.flatnonzero(global_masks[i]))
+        rep_probs.append(p)
+    # full state on the finest replicated level: owned slices, all-reduced
+    cslab = slabs[first].halved()
+    uc_local = torch.empty(cslab.n_dofs, dtype=torch.float64, device="cuda")
+    coarse_local = Problem(sub_box(global_meshes[first - 1], cslab.axis, cslab.c0, cslab.c1), degree, mat,
+                           has_top_face=not cslab.has_upper)
+    cmask = np.ascontiguousarray(cslab.local(global_masks[first - 1]))
+    coarse_local.constraints = ConstraintSet.from_dofs(coarse_local.n_dofs, np.flatnonzero(cmask))
+    check(lib().hf_inject(coarse_local._space, dps[first].local._space, dv.ptr(u[first]), dv.ptr(uc_local), 0,
+                          dv.stream()))
+    ufull = torch.zeros(cslab.n_global_dofs, dtype=torch.float64, device="cuda")
+    o = cslab.owned
+    ufull[cslab.dof_offset + o.start:cslab.dof_offset + o.stop] = uc_local[o]
+    comm.allreduce_(ufull)
+    rep_transfers = build_transfers(rep_probs)
+    rep_levels = build_level_operators(rep_probs, ufull, strategy, seed)
+    replicated = GMGPreconditioner(rep_levels, rep_transfers)
+    bridge = TransferOperator(coarse_local, dps[first].local)
+    gmg = DistGMG(levels, transfers, bridge, replicated, cslab, comm)
+    gmg._keep = (coarse_local, rep_probs)
+    fine_op = levels[-1].op
+    return gmg, dps[nlev - 1], fine_op

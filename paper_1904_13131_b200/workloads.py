@@ -47,19 +47,23 @@ def lattice_1d(m: int, degree: int) -> np.ndarray:
     return out
 
 
-def clamp_weighted_sine(dim: int, m: int, degree: int, phases: np.ndarray, amp: float, clamp_axis: int) -> np.ndarray:
-    """u_c = amp X_clamp prod_a sin(pi X_a + phi[c,a]) on the node lattice, node-blocked."""
-    x1 = lattice_1d(m, degree)
-    n = len(x1)
-    u = np.empty((n,) * dim + (dim,))  # array axes (z, y, x) / (y, x)
+def clamp_weighted_sine(dim: int, m, degree: int, phases: np.ndarray, amp: float, clamp_axis: int) -> np.ndarray:
+    """u_c = amp X_clamp prod_a sin(pi X_a + phi[c,a]) on the node lattice, node-blocked.
+
+    ``m`` is the cells per axis (an int for the unit cube, or a per-axis tuple:
+    each axis' lattice spans [0, 1])."""
+    ms = (m,) * dim if np.isscalar(m) else tuple(m)
+    x1 = [lattice_1d(mm, degree) for mm in ms]
+    shape_all = tuple(len(x1[a]) for a in reversed(range(dim)))
+    u = np.empty(shape_all + (dim,))  # array axes (z, y, x) / (y, x)
     for c in range(dim):
-        f = np.ones((n,) * dim)
+        f = np.ones(shape_all)
         for a in range(dim):
             shape = [1] * dim
-            shape[dim - 1 - a] = n
-            fac = np.sin(np.pi * x1 + phases[c, a])
+            shape[dim - 1 - a] = len(x1[a])
+            fac = np.sin(np.pi * x1[a] + phases[c, a])
             if a == clamp_axis:
-                fac = fac * x1
+                fac = fac * x1[a]
             f = f * fac.reshape(shape)
         u[..., c] = amp * f
     return u.reshape(-1)
@@ -117,6 +121,75 @@ def make_workload(cfg_id: int, seed: int = 0, amp: float = AMP_VMULT, levels: bo
     if with_x:
         wl.x = rng.standard_normal(wl.fine.n_dofs)
     return wl
+
+
+@dataclass
+class HostWorkload:
+    """Host-only description of a BASELINE config (for the multi-GPU path: every
+    rank derives its slab from the same global meshes, masks and vectors)."""
+
+    cfg: dict
+    meshes: list        # global mesh per level, coarsest first
+    masks: list         # global constraint mask per level
+    ubar: np.ndarray    # global linearisation point (finest level)
+    x: np.ndarray | None
+
+
+def host_workload(cfg_id: int, seed: int = 0, amp: float = AMP_VMULT, levels: bool = False, m: int | None = None,
+                  coarsest: int | None = None, with_x: bool = True, stack: int = 1) -> HostWorkload:
+    """Same draws as ``make_workload``; ``stack`` > 1 stacks copies of the cell
+    layers along the last axis (weak-scaling meshes of ``stack`` GPUs)."""
+    from .fespace import build_dof_map
+
+    cfg = dict(CONFIGS[cfg_id])
+    if m is not None:
+        cfg["m"] = m
+    if coarsest is not None:
+        cfg["coarsest"] = coarsest
+    dim, p = cfg["dim"], cfg["degree"]
+    rng = np.random.default_rng(seed)
+    centres = rng.random((cfg["n_inc"], dim))
+    phases = 2.0 * np.pi * rng.random((dim, dim))
+    ms = [cfg["m"]]
+    if levels:
+        while ms[0] // 2 >= cfg["coarsest"] and ms[0] % 2 == 0:
+            ms.insert(0, ms[0] // 2)
+    spec = [(c, cfg["radius"]) for c in centres]
+    meshes, masks = [], []
+    for mm in ms:
+        mesh = build_benchmark_mesh(dim, mm, spec, side=1.0)
+        if stack > 1:
+            mesh = stack_mesh(mesh, stack)
+        dm = build_dof_map(mesh, p, dim)
+        dofs = [face_dofs(dm, cfg["clamp_axis"], 0)]
+        if cfg.get("top_z"):
+            dofs.append(face_dofs(dm, dim - 1, 1, components=[dim - 1]))
+        mask = np.zeros(dm.n_dofs, dtype=bool)
+        mask[np.concatenate(dofs)] = True
+        meshes.append(mesh)
+        masks.append(mask)
+    # stacked meshes: the same smooth field over the whole stack (its last axis mapped onto [0, 1])
+    ubar = clamp_weighted_sine(dim, meshes[-1].cells, p, phases, amp, cfg["clamp_axis"])
+    n_dofs = int(np.prod([c * p + 1 for c in meshes[-1].cells])) * dim
+    x = rng.standard_normal(n_dofs) if with_x else None
+    return HostWorkload(cfg, meshes, masks, ubar, x)
+
+
+def stack_mesh(mesh, k: int):
+    """``k`` copies of a box mesh stacked along the last axis (shifted by its side)."""
+    from dataclasses import replace
+
+    d = mesh.dim
+    vg = mesh.vertices.reshape(tuple(c + 1 for c in reversed(mesh.cells)) + (d,))
+    parts = []
+    for i in range(k):
+        v = vg[: -1 if i < k - 1 else None].copy()
+        v[..., d - 1] += i * mesh.side
+        parts.append(v)
+    verts = np.concatenate(parts, axis=0).reshape(-1, d)
+    mat = np.tile(mesh.material_id.reshape(mesh.cells[-1], -1), (k, 1)).reshape(-1)
+    cells = tuple(mesh.cells[:-1]) + (mesh.cells[-1] * k,)
+    return replace(mesh, cells=cells, vertices=np.ascontiguousarray(verts), material_id=mat)
 
 
 def algorithmic_bytes(strategy: str, dim: int, n_dofs: int, n_qp: int) -> int:
