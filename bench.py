@@ -1,15 +1,27 @@
 """Benchmark: tangent vmult GDoF/s (fp64) of the matrix-free Neo-Hookean
-operator on B200, plus the GMG-CG Newton-iteration time.
+operator on B200, plus the GMG-CG Newton-step time.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one MatrixFreeTangent.apply (tensor4 cache, the paper's
-"Algorithm 3") on BASELINE config 2 (3D 32^3 Q2, 823,875 DoFs, seeded
-synthetic inputs).  L2 is flushed (256 MiB write) before every
-timed step; each step is bracketed by CUDA events on the launching stream.
-Extra keys report the other caching variants, config 3 (16^3 Q4) and one
-Newton iteration of config 4.  Under torchrun every rank runs an independent
-replica (weak scaling, no data-path collective), timed as the max over ranks.
+One step = one tangent application (tensor4 cache, the paper's "Algorithm 3")
+through ``MatrixFreeTangent.apply`` semantics: y = mask ? x : 0, the cell
+kernel, and for N > 1 the interface exchange.  Workload: BASELINE config 2
+(3D 32^3 Q2, 823,875 DoFs per GPU, seeded synthetic inputs).
+
+* N = 1: the config-2 mesh itself.
+* N > 1 (torchrun, one rank per GPU, NCCL): weak scaling over slabs.  The
+  global mesh is N config-2 cubes stacked along z (32 x 32 x 32N cells); each
+  rank owns one 32-layer slab.  The interface reverse-add (NCCL send/recv +
+  hf_halo_add) is inside the timed step.  ``value`` = global DoFs / the max
+  over ranks of the step time.
+
+L2 is flushed (256 MiB write) before every timed step; steps are bracketed by
+CUDA events on the launching stream.  ``roofline`` uses the kernel-only event
+pair around the cell kernel.  At N = 1 rank 0 adds: the other caching
+variants, config 3 (16^3 Q4), one config-4 Newton iteration (64^3, GMG levels
+4..64), the measured fp64 peak, and the CPU baseline (the oracle port).
+``--impl reference`` times the reference algorithm's CPU port (oracle/) on all
+host cores: the reference is pure Python and absent on the GPU box.
 """
 
 from __future__ import annotations
@@ -27,15 +39,26 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "tangent vmult GDoF/s (fp64) + GMG-CG Newton-step time at 1/2/4/8 B200"
+KERNEL = "hf::k_apply_line<3,3,TENSOR4>"
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
-        return float(pk["hbm_gbs"]), "measured"
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _traffic():
+    """DRAM bytes per launch of the headline kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t if t.get("kernel") == KERNEL else None
+    except Exception:
+        return None
 
 
 class Clocks:
@@ -52,8 +75,9 @@ class Clocks:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.2)
         except Exception:
             self.p = None
         return self
@@ -62,7 +86,7 @@ class Clocks:
         self.rows = []
         if self.p is None:
             return
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.p.terminate()
         out, _ = self.p.communicate(timeout=5)
         for line in out.strip().splitlines():
@@ -89,8 +113,9 @@ def _dist():
     return ws, rank, local
 
 
-def _time_apply(op, x, y, steps, warmup, flush):
-    """Per step: flush L2, init y (mask copy), apply kernel; events around each."""
+def _time_steps(local_op, x, y, steps, warmup, flush, exchange=None, flush_l2=True):
+    """Per step: [flush L2], e0, y = mask ? x : 0, k0, cell kernel, k1, [interface add], e1.
+    Returns (mean step ms, mean kernel ms, launches per step)."""
     import torch
 
     from paper_1904_13131_b200 import _lib
@@ -98,101 +123,151 @@ def _time_apply(op, x, y, steps, warmup, flush):
 
     L = _lib.lib()
     n = x.numel()
-    mask = op.problem.mask_ptr()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
-    for _ in range(warmup):
-        flush.zero_()
-        op.apply_into(x, y)
-    torch.cuda.synchronize()
-    for k in range(steps):
-        flush.zero_()
-        ev[k][0].record()
+    mask = local_op.problem.mask_ptr()
+
+    def one(ev=None):
+        if ev:
+            ev[0].record()
         _lib.check(L.hf_fill_masked(n, dv.ptr(y), dv.ptr(x), mask, 0.0, dv.stream()))
-        ev[k][1].record()
-        op.apply_raw(x, y)
-        ev[k][2].record()
+        if ev:
+            ev[1].record()
+        local_op.apply_raw(x, y)
+        if ev:
+            ev[2].record()
+        if exchange is not None:
+            exchange.add(y)
+        if ev:
+            ev[3].record()
+
+    for _ in range(warmup):
+        if flush_l2:
+            flush.zero_()
+        one()
     torch.cuda.synchronize()
-    step_ms = [ev[k][0].elapsed_time(ev[k][2]) for k in range(steps)]
-    kern_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(steps)]
-    return float(np.mean(step_ms)), float(np.mean(kern_ms)), 2 * steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    for k in range(steps):
+        if flush_l2:
+            flush.zero_()
+        one(evs[k])
+    torch.cuda.synchronize()
+    step = [e[0].elapsed_time(e[3]) for e in evs]
+    kern = [e[1].elapsed_time(e[2]) for e in evs]
+    launches = 2 + (len(exchange.peers) if exchange is not None else 0)
+    return float(np.mean(step)), float(np.mean(kern)), launches
 
 
-def _e2e(op, x_np, steps, warmup):
-    """Public API with pinned host buffers: H2D + apply + D2H inside the timed region."""
+def _e2e(apply_into, x_host: np.ndarray, steps, warmup):
+    """Through the public apply: pinned H2D of x, tangent apply, D2H of y, every step."""
     import torch
 
-    xh = torch.from_numpy(x_np.copy()).pin_memory()
+    xh = torch.from_numpy(x_host.copy()).pin_memory()
     yh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty(xh.shape, dtype=torch.float64, device="cuda")
+    yd = torch.empty_like(xd)
+
+    def one():
+        xd.copy_(xh, non_blocking=True)
+        apply_into(xd, yd)
+        yh.copy_(yd, non_blocking=True)
+
     for _ in range(warmup):
-        op.apply(xh, out=yh)
+        one()
     torch.cuda.synchronize()
     t = []
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        op.apply(xh, out=yh)
+        one()
         e1.record()
         torch.cuda.synchronize()
         t.append(e0.elapsed_time(e1))
     return float(np.mean(t)), xh.numel() * 8, yh.numel() * 8
 
 
-def cpu_baseline(cfg_id=2, strategy="tensor4", budget_s=20.0, threads=1):
-    """Oracle (numpy port of the reference) on a bounded sample: cache build +
-    as many applies as fit in the budget (at least one)."""
-    from threadpoolctl import threadpool_limits
+def fp64_peak():
+    """Measured DFMA throughput (TFLOP/s): 148 x 8 blocks x 256 threads x 8 chains."""
+    import torch
 
+    from paper_1904_13131_b200 import _lib
+    from paper_1904_13131_b200 import device as dv
+
+    L = _lib.lib()
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, threads, iters = nsm * 8, 256, 20000
+    for _ in range(2):
+        _lib.check(L.hf_probe_dfma(iters, blocks, threads, dv.ptr(sink), dv.stream()))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _lib.check(L.hf_probe_dfma(iters, blocks, threads, dv.ptr(sink), dv.stream()))
+    e1.record()
+    torch.cuda.synchronize()
+    return 16.0 * iters * blocks * threads / (e0.elapsed_time(e1) * 1e-3) / 1e12
+
+
+def _oracle_apply(cfg_id=2, strategy="tensor4"):
+    """The reference algorithm's CPU port (oracle/) set up on a config: returns (apply, x, DoFs)."""
     from oracle import hf_oracle as O
-    from paper_1904_13131_b200.workloads import CONFIGS, MATERIAL, clamp_weighted_sine, AMP_VMULT
-    from paper_1904_13131_b200.mesh import build_benchmark_mesh
-    from paper_1904_13131_b200.fespace import build_dof_map, face_dofs
+    from paper_1904_13131_b200.workloads import AMP_VMULT, MATERIAL, host_workload
 
-    cfg = CONFIGS[cfg_id]
-    rng = np.random.default_rng(0)
-    centres = rng.random((cfg["n_inc"], cfg["dim"]))
-    phases = 2.0 * np.pi * rng.random((cfg["dim"], cfg["dim"]))
-    d, m, p = cfg["dim"], cfg["m"], cfg["degree"]
-    mesh = build_benchmark_mesh(d, m, [(c, cfg["radius"]) for c in centres], side=1.0)
+    hw = host_workload(cfg_id, seed=0, amp=AMP_VMULT)
+    mesh = hw.meshes[-1]
     inc = mesh.material_id == 1
     mu = np.where(inc, MATERIAL.inclusion.mu, MATERIAL.matrix.mu)
     lam = np.where(inc, MATERIAL.inclusion.lam, MATERIAL.matrix.lam)
-    dm = build_dof_map(mesh, p, d)
-    mask = np.zeros(dm.n_dofs, dtype=bool)
-    mask[face_dofs(dm, cfg["clamp_axis"], 0)] = True
-    ubar = clamp_weighted_sine(d, m, p, phases, AMP_VMULT, cfg["clamp_axis"])
-    x = rng.standard_normal(dm.n_dofs)
+    prob = O.OProblem(mesh.dim, hw.cfg["degree"], mesh.cells, mesh.vertices, mu, lam, hw.masks[-1])
+    prob.geometry()
+    op = O.Tangent(prob, hw.ubar, strategy)
+    return op.apply, hw.x, prob.n_dofs
+
+
+def cpu_baseline(cfg_id=2, strategy="tensor4", budget_s=20.0, threads=1):
+    """Oracle port on a bounded sample: setup, 1 warm-up apply (bench.py:206
+    convention), then applies until the budget (>= 1, <= 10).  Returns
+    (GDoF/s, s per apply, applies, DoFs)."""
+    from threadpoolctl import threadpool_limits
+
     with threadpool_limits(threads):
-        prob = O.OProblem(d, p, mesh.cells, mesh.vertices, mu, lam, mask)
-        prob.geometry()
-        op = O.Tangent(prob, ubar, strategy)
+        apply, x, ndofs = _oracle_apply(cfg_id, strategy)
+        apply(x)
         t0 = time.perf_counter()
         n = 0
-        while True:
-            op.apply(x)
+        while n < 1 or (time.perf_counter() - t0 < budget_s and n < 10):
+            apply(x)
             n += 1
-            if time.perf_counter() - t0 > budget_s / 2 or n >= 10:
-                break
         dt = (time.perf_counter() - t0) / n
-    return dm.n_dofs / dt / 1e9, dt, n, dm.n_dofs
+    return ndofs / dt / 1e9, dt, n, ndofs
 
 
 def run_reference(args):
+    """The reference algorithm's CPU implementation (the oracle port; the reference
+    is pure Python and absent on the GPU box) on all host cores; one step = one
+    apply of config 2, W warm-up steps, then up to K timed steps (bounded to ~90 s)."""
+    from threadpoolctl import threadpool_limits
+
     ws, rank, _ = _dist()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    vals = []
-    for _ in range(max(args.steps, 1)):
-        v, dt, n, ndofs = cpu_baseline(2, "tensor4", budget_s=6.0, threads=threads)
-        vals.append(v)
-    v = float(np.mean(vals))
+    with threadpool_limits(threads):
+        apply, x, ndofs = _oracle_apply(2, "tensor4")
+        for _ in range(min(args.warmup, 1)):
+            apply(x)
+        times = []
+        while len(times) < max(args.steps, 1) and sum(times) < 90.0:
+            t0 = time.perf_counter()
+            apply(x)
+            times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    v = ndofs / dt / 1e9
     line = {"metric": METRIC, "value": v, "unit": "GDoF/s", "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ndofs / v / 1e6, "higher_is_better": True,
+            "steps": len(times), "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "cfg2 3D 32^3 Q2 tensor4 tangent vmult (823,875 DoFs)", "strategy": "tensor4"},
             "cpu_baseline": {"value": v, "unit": "GDoF/s", "cores": threads, "kind": "port",
-                             "sample": f"oracle/hf_oracle.py (numpy port of the reference) apply, "
-                                       f"{n} applies after a cache build per step"},
+                             "sample": "oracle/hf_oracle.py (numpy restatement of the reference operators.py:331-393, "
+                                       f"pinned to reference golden vectors): {len(times)} timed applies of cfg2 after "
+                                       "1 warm-up"},
             "e2e": {"value": v, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -209,102 +284,116 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     from paper_1904_13131_b200 import MatrixFreeTangent
-    from paper_1904_13131_b200.workloads import algorithmic_bytes, make_workload, meter_flops
+    from paper_1904_13131_b200.distributed import DistProblem, DistributedTangent, Slab, TorchComm, slab_ranges
+    from paper_1904_13131_b200.workloads import MATERIAL, algorithmic_bytes, host_workload, make_workload, meter_flops
 
     hbm, peak_kind = _peaks()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    wl = make_workload(2, seed=rank)
-    p = wl.fine
-    x = torch.from_numpy(wl.x).cuda()
+    exchange = None
+    if ws == 1:
+        wl = make_workload(2, seed=0)
+        prob, ubar, x_host = wl.fine, wl.ubar, wl.x
+        n_global = prob.n_dofs
+        make_op = lambda s: MatrixFreeTangent(prob, ubar, s)  # noqa: E731
+        public = None
+    else:
+        comm = TorchComm()
+        hw = host_workload(2, seed=0, stack=ws)
+        cells = hw.meshes[-1].cells
+        slab = Slab(3, 2, cells, *slab_ranges(cells[-1], ws)[rank])
+        dp = DistProblem(hw.meshes[-1], 2, MATERIAL, slab, comm, hw.masks[-1])
+        prob, ubar, x_host = dp.local, np.ascontiguousarray(slab.local(hw.ubar)), np.ascontiguousarray(slab.local(hw.x))
+        n_global = slab.n_global_dofs
+        exchange = dp.exchange
+        public = DistributedTangent(dp, ubar, "tensor4")
+        make_op = lambda s: public.local if s == "tensor4" else MatrixFreeTangent(prob, ubar, s)  # noqa: E731
+    x = torch.from_numpy(x_host).cuda()
     y = torch.empty_like(x)
-    nqp = p.mesh.n_elements * p.n_qpoints_per_cell
-    variants = {}
-    head = None
-    for s in ("tensor4", "tensor2", "scalar"):
-        op = MatrixFreeTangent(p, wl.ubar, s)
-        if s == "tensor4":
-            if ws > 1:
-                torch.distributed.barrier()
-            torch.cuda.synchronize()
-            with Clocks(torch.cuda.current_device()) as clk:
-                step_ms, kern_ms, launches = _time_apply(op, x, y, args.steps, args.warmup, flush)
-            torch.cuda.synchronize()
-            if ws > 1:
-                t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device="cuda")
-                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-                step_ms, kern_ms = t.tolist()
-            head = (op, step_ms, kern_ms, launches, clk.summary())
-        else:
-            sm, km, _ = _time_apply(op, x, y, max(args.steps // 2, 3), 3, flush)
-            ab = algorithmic_bytes(s, 3, p.n_dofs, nqp)
-            variants[s] = {"GDoF_s": p.n_dofs / sm / 1e6, "kernel_ms": km, "step_ms": sm,
-                           "achieved_GBs": ab / km / 1e6, "frac_hbm": ab / km / 1e6 / hbm,
-                           "meter_GFLOP_s": meter_flops(3, 2, p.mesh.n_elements, s) / km / 1e6}
-        del op
-    op, step_ms, kern_ms, launches, clocks = head
-    ab = algorithmic_bytes("tensor4", 3, p.n_dofs, nqp)
-    variants["tensor4"] = {"GDoF_s": p.n_dofs / step_ms / 1e6, "kernel_ms": kern_ms, "step_ms": step_ms,
-                           "achieved_GBs": ab / kern_ms / 1e6, "frac_hbm": ab / kern_ms / 1e6 / hbm,
-                           "meter_GFLOP_s": meter_flops(3, 2, p.mesh.n_elements, "tensor4") / kern_ms / 1e6}
-    e2e_ms, h2d, d2h = _e2e(op, wl.x, max(args.steps // 2, 3), 2)
-    value = ws * p.n_dofs / step_ms / 1e6  # GDoF/s over all ranks
-    extra = {}
-    if not args.no_extra and rank == 0:
-        extra = _extras(args, hbm)
-    line = {"metric": METRIC, "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg2 3D 32^3 Q2 tensor4 tangent vmult (823,875 DoFs)", "strategy": "tensor4",
-                       "l2": "256 MiB flush before every timed step", "parallelism": f"replicas x{ws}"},
+    nqp = prob.mesh.n_elements * prob.n_qpoints_per_cell
+    op = make_op("tensor4")
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with Clocks(torch.cuda.current_device()) as clk:
+        step_ms, kern_ms, launches = _time_steps(op, x, y, args.steps, args.warmup, flush, exchange)
+    torch.cuda.synchronize()
+    if ws > 1:
+        t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        step_ms, kern_ms = t.tolist()
+    ab = algorithmic_bytes("tensor4", 3, prob.n_dofs, nqp)
+    apply_into = public.apply_into if public is not None else op.apply_into
+    e2e_ms, h2d, d2h = _e2e(apply_into, x_host, max(args.steps // 2, 3), args.warmup)
+    if ws > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = t.item()
+    traffic = _traffic()
+    line = {"metric": METRIC, "value": n_global / step_ms / 1e6, "unit": "GDoF/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": ("cfg2 3D 32^3 Q2 tensor4 tangent vmult (823,875 DoFs)" if ws == 1 else
+                                    f"cfg2 weak-scaled: 32x32x{32 * ws} Q2 cells, one 32-layer slab per GPU, "
+                                    f"{n_global} DoFs"),
+                       "strategy": "tensor4", "dofs_per_gpu": int(prob.n_dofs),
+                       "l2": "256 MiB write flush before every timed step",
+                       "parallelism": "single GPU" if ws == 1 else f"slab decomposition x{ws} (NCCL interface add)"},
             "roofline": {"bound": "hbm", "achieved": ab / kern_ms / 1e6, "peak": hbm, "unit": "GB/s",
-                         "frac": ab / kern_ms / 1e6 / hbm, "traffic": None, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": ab, "kernel": "hf::k_apply_line<3,3,TENSOR4>"},
-            "e2e": {"value": ws * p.n_dofs / e2e_ms / 1e6, "unit": "GDoF/s", "h2d_bytes_per_step": h2d,
+                         "frac": ab / kern_ms / 1e6 / hbm, "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "peak_source": peak_kind, "algorithmic_bytes_per_launch": ab,
+                         "kernel_ms": kern_ms, "kernel": KERNEL},
+            "e2e": {"value": n_global / e2e_ms / 1e6, "unit": "GDoF/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": launches, "clocks": clocks, "variants": variants}
-    line.update(extra)
+            "gpu_launches": launches * args.steps, "clocks": clk.summary()}
+    if rank == 0 and ws == 1 and not args.no_extra:
+        line.update(_extras(args, hbm, prob, ubar, x, y, flush, nqp))
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, dt, n, _ = cpu_baseline(2, "tensor4", budget_s=20.0, threads=1)
         line["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": 1, "kind": "port",
-                                "sample": f"oracle numpy port, cfg2 tensor4 apply x{n} (1 BLAS thread)"}
+                                "sample": f"oracle numpy port of the reference apply, cfg2 tensor4, {n} applies "
+                                          f"after 1 warm-up ({dt:.2f} s each, 1 BLAS thread)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 
 
-def _extras(args, hbm):
-    """Config 3 (16^3 Q4) vmult and one config-4 Newton iteration."""
-    import torch
-
+def _extras(args, hbm, prob, ubar, x, y, flush, nqp):
+    """Other caching variants (cfg 2), config 3 (16^3 Q4), fp64 peak, one config-4 Newton iteration."""
     from paper_1904_13131_b200 import MatrixFreeTangent
-    from paper_1904_13131_b200.workloads import algorithmic_bytes, make_workload
+    from paper_1904_13131_b200.workloads import algorithmic_bytes, make_workload, meter_flops
 
     out = {}
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    wl = make_workload(3, seed=0)
-    p = wl.fine
-    x = torch.from_numpy(wl.x).cuda()
-    y = torch.empty_like(x)
-    nqp = p.mesh.n_elements * p.n_qpoints_per_cell
-    c3 = {}
-    for s in ("tensor4", "tensor2", "scalar"):
-        op = MatrixFreeTangent(p, wl.ubar, s)
-        sm, km, _ = _time_apply(op, x, y, 10, 3, flush)
-        ab = algorithmic_bytes(s, 3, p.n_dofs, nqp)
-        c3[s] = {"GDoF_s": p.n_dofs / sm / 1e6, "kernel_ms": km, "achieved_GBs": ab / km / 1e6,
-                 "frac_hbm": ab / km / 1e6 / hbm}
-        del op
-    out["cfg3_q4"] = c3
+    fp64 = fp64_peak()
+    out["fp64_peak_tflops_measured"] = fp64
+
+    def variant(p, ub, xx, yy, s, nq):
+        op = MatrixFreeTangent(p, ub, s)
+        sm, km, _ = _time_steps(op, xx, yy, max(args.steps // 2, 5), 3, flush)
+        ab = algorithmic_bytes(s, 3, p.n_dofs, nq)
+        fl = meter_flops(3, p.degree, p.mesh.n_elements, s)
+        return {"GDoF_s": p.n_dofs / sm / 1e6, "kernel_ms": km, "step_ms": sm, "achieved_GBs": ab / km / 1e6,
+                "frac_hbm": ab / km / 1e6 / hbm, "meter_TFLOP_s": fl / km / 1e9, "frac_fp64": fl / km / 1e9 / fp64}
+
+    out["variants"] = {s: variant(prob, ubar, x, y, s, nqp) for s in ("tensor4", "tensor2", "scalar")}
+    wl3 = make_workload(3, seed=0)
+    p3 = wl3.fine
+    import torch
+
+    x3 = torch.from_numpy(wl3.x).cuda()
+    y3 = torch.empty_like(x3)
+    nq3 = p3.mesh.n_elements * p3.n_qpoints_per_cell
+    out["cfg3_q4"] = {s: variant(p3, wl3.ubar, x3, y3, s, nq3) for s in ("tensor4", "tensor2", "scalar")}
     if not args.no_newton:
         out["newton"] = _newton_iteration()
     return out
 
 
 def _newton_iteration():
-    """Time the first Newton iteration of load step 1 of config 4 (64^3 Q2,
-    levels 4..64, prescribed top displacement): tangent + GMG build, CG to
-    1e-6, residual."""
+    """First Newton iteration of load step 1 of config 4 (64^3 Q2, levels 4..64,
+    prescribed top displacement): tangent + GMG build, CG to 1e-6
+    (NewtonSettings.linear_rel_tol, solver.py:85), residual.  Run twice; the
+    second (warm) run is reported."""
     import torch
 
     from paper_1904_13131_b200 import MatrixFreeTangent, build_gmg, build_transfers, cg, compute_residual
@@ -314,28 +403,31 @@ def _newton_iteration():
     wl = make_workload(4, seed=0, levels=True, with_x=False)
     probs = wl.problems
     fine = probs[-1]
-    d = 3
     X = node_coordinates(fine.mesh, fine.dofmap)
-    u = torch.zeros(fine.n_dofs, dtype=torch.float64, device="cuda")
-    u.view(-1, d)[:, 2] += (-0.05 / 5) * torch.from_numpy(X[:, 2]).cuda()
     transfers = build_transfers(probs)
-    res = compute_residual(fine, u)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    op = MatrixFreeTangent(fine, u, "tensor4")
-    gmg = build_gmg(probs, u, "tensor4", seed=0, transfers=transfers, keep_constrained=True)
-    torch.cuda.synchronize()
-    t1 = time.perf_counter()
-    du, rep = cg(op, -res, rel_tol=1e-6, preconditioner=gmg)
-    torch.cuda.synchronize()
-    t2 = time.perf_counter()
-    u += du
-    res = compute_residual(fine, u)
-    torch.cuda.synchronize()
-    t3 = time.perf_counter()
-    return {"workload": "cfg4 64^3 Q2 levels 4..64, load step 1, iteration 1", "n_dofs": fine.n_dofs,
-            "newton_iteration_s": t3 - t0, "setup_s": t1 - t0, "cg_s": t2 - t1, "cg_iterations": rep.iterations,
-            "s_per_cg_iteration": (t2 - t1) / max(rep.iterations, 1)}
+    rec = None
+    for _ in range(2):
+        u = torch.zeros(fine.n_dofs, dtype=torch.float64, device="cuda")
+        u.view(-1, 3)[:, 2] += (-0.05 / 5) * torch.from_numpy(X[:, 2] / X[:, 2].max()).cuda()
+        res = compute_residual(fine, u)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op = MatrixFreeTangent(fine, u, "tensor4")
+        gmg = build_gmg(probs, u, "tensor4", seed=0, transfers=transfers, keep_constrained=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        du, rep = cg(op, -res, rel_tol=1e-6, preconditioner=gmg)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        u += du
+        res = compute_residual(fine, u)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        rec = {"workload": "cfg4 64^3 Q2 levels 4..64, load step 1, Newton iteration 1", "n_dofs": fine.n_dofs,
+               "newton_iteration_s": t3 - t0, "setup_s": t1 - t0, "cg_s": t2 - t1, "cg_iterations": rep.iterations,
+               "s_per_cg_iteration": (t2 - t1) / max(rep.iterations, 1)}
+        del op, gmg
+    return rec
 
 
 def main():
@@ -348,8 +440,7 @@ def main():
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
     else:

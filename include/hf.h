@@ -160,6 +160,9 @@ HF_API int hf_cg_update_p(long long n, double* p, const double* z, const double*
 /* z = inv_d r; out_dev[0] = r . z */
 HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, const double* inv_d, double* out_dev,
                          void* stream);
+/* diagnostic: blocks x threads threads run 8 independent chains of `iters`
+ * DFMAs (16 * iters flops per thread) -- the measured fp64 roofline peak */
+HF_API int hf_probe_dfma(long long iters, int blocks, int threads, double* sink_dev, void* stream);
 /* reverse halo add of a slab interface (multi-GPU; no reference
  * analogue -- the paper's MPI ghost exchange):
  * y[i] += recv[i] where mask[i] == 0 */

@@ -69,6 +69,7 @@ _SIGS = {
     "hf_jacobi_dot": (I, [P, LL, P, P, P, P, P]),
     "hf_axpby": (I, [LL, D, P, D, P, P]),
     "hf_halo_add": (I, [LL, P, P, P, P]),
+    "hf_probe_dfma": (I, [LL, I, I, P, P]),
 }
 
 

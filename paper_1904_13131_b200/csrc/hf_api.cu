@@ -620,6 +620,13 @@ HF_API int hf_fill_masked(long long n, double* y, const double* x, const unsigne
   return HF_OK;
 }
 
+HF_API int hf_probe_dfma(long long iters, int blocks, int threads, double* sink_dev, void* stream) {
+  if (!sink_dev || iters < 1 || blocks < 1 || threads < 32) return fail(HF_ERR_ARG, "bad probe arguments");
+  k_probe_dfma<<<blocks, threads, 0, S(stream)>>>(iters, sink_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
 HF_API int hf_halo_add(long long n, double* y, const double* recv, const unsigned char* mask, void* stream) {
   if (!y || !recv || !mask) return fail(HF_ERR_ARG, "null argument");
   if (n <= 0) return HF_OK;

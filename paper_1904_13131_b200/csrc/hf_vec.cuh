@@ -56,6 +56,23 @@ __global__ void k_halo_add(long long n, double* __restrict__ y, const double* __
     if (!mask[i]) y[i] += recv[i];
 }
 
+// fp64 throughput probe (the denominator of the fp64 roofline; MEASURED_PEAKS
+// has no fp64 entry): 8 independent DFMA chains per thread
+__global__ void k_probe_dfma(long long iters, double* sink) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + 1e-3 * (threadIdx.x + k);
+  const double m = 0.999999, c = 1e-7;
+  for (long long i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) sink[0] = s;  // keep the chains alive
+}
+
 inline unsigned red_blocks(long long n) {
   long long b = (n + RED_THREADS * 4 - 1) / (RED_THREADS * 4);
   if (b < 1) b = 1;

@@ -507,7 +507,8 @@ class DistGMG:
 
 
 def build_dist_gmg(global_meshes: list, degree: int, mat: Material, global_masks: list, u_fine_local, comm,
-                   strategy: str = "tensor4", seed: int = 0, min_cells: int = 2):
+                   strategy: str = "tensor4", seed: int = 0, min_cells: int = 2, keep_constrained: bool = False,
+                   fine_dp: "DistProblem | None" = None):
     """Distributed analogue of build_gmg (multigrid.py:372-382).
 
     ``global_meshes``/``global_masks``: every level, coarsest first.  Returns
@@ -518,14 +519,15 @@ def build_dist_gmg(global_meshes: list, degree: int, mat: Material, global_masks
     first = next(i for i, s in enumerate(slabs) if s is not None)
     if first == 0:
         raise ValueError("the coarsest level must be replicated (min_cells too small for the hierarchy)")
-    dps = {i: DistProblem(global_meshes[i], degree, mat, slabs[i], comm, global_masks[i])
+    dps = {i: (fine_dp if (i == nlev - 1 and fine_dp is not None) else
+               DistProblem(global_meshes[i], degree, mat, slabs[i], comm, global_masks[i]))
            for i in range(first, nlev)}
     # injection of the fine state down the distributed levels (multigrid.py:76-92)
     u = {nlev - 1: dv.as_dev(u_fine_local)}
     for lvl in range(nlev - 1, first, -1):
         uc = torch.empty(dps[lvl - 1].n_dofs, dtype=torch.float64, device="cuda")
-        check(lib().hf_inject(dps[lvl - 1].local._space, dps[lvl].local._space, dv.ptr(u[lvl]), dv.ptr(uc), 0,
-                              dv.stream()))
+        check(lib().hf_inject(dps[lvl - 1].local._space, dps[lvl].local._space, dv.ptr(u[lvl]), dv.ptr(uc),
+                              int(keep_constrained), dv.stream()))
         u[lvl - 1] = uc
     levels = [DistLevel(dps[i], u[i], strategy, seed + 7919 * i, i) for i in range(first, nlev)]
     transfers = [TransferOperator(dps[i].local, dps[i + 1].local) for i in range(first, nlev - 1)]
@@ -542,14 +544,14 @@ def build_dist_gmg(global_meshes: list, degree: int, mat: Material, global_masks
                            has_top_face=not cslab.has_upper)
     cmask = np.ascontiguousarray(cslab.local(global_masks[first - 1]))
     coarse_local.constraints = ConstraintSet.from_dofs(coarse_local.n_dofs, np.flatnonzero(cmask))
-    check(lib().hf_inject(coarse_local._space, dps[first].local._space, dv.ptr(u[first]), dv.ptr(uc_local), 0,
-                          dv.stream()))
+    check(lib().hf_inject(coarse_local._space, dps[first].local._space, dv.ptr(u[first]), dv.ptr(uc_local),
+                          int(keep_constrained), dv.stream()))
     ufull = torch.zeros(cslab.n_global_dofs, dtype=torch.float64, device="cuda")
     o = cslab.owned
     ufull[cslab.dof_offset + o.start:cslab.dof_offset + o.stop] = uc_local[o]
     comm.allreduce_(ufull)
     rep_transfers = build_transfers(rep_probs)
-    rep_levels = build_level_operators(rep_probs, ufull, strategy, seed)
+    rep_levels = build_level_operators(rep_probs, ufull, strategy, seed, keep_constrained)
     replicated = GMGPreconditioner(rep_levels, rep_transfers)
     bridge = TransferOperator(coarse_local, dps[first].local)
     gmg = DistGMG(levels, transfers, bridge, replicated, cslab, comm)
