@@ -114,45 +114,36 @@ def _dist():
 
 
 def _time_steps(local_op, x, y, steps, warmup, flush, exchange=None, flush_l2=True):
-    """Per step: [flush L2], e0, y = mask ? x : 0, k0, cell kernel, k1, [interface add], e1.
+    """Per step: [flush L2], e0, tangent apply (ONE launch: y = mask ? x : 0 fused
+    into the cell kernel), e1, [interface add], e2.
     Returns (mean step ms, mean kernel ms, launches per step)."""
     import torch
-
-    from paper_1904_13131_b200 import _lib
-    from paper_1904_13131_b200 import device as dv
-
-    L = _lib.lib()
-    n = x.numel()
-    mask = local_op.problem.mask_ptr()
 
     def one(ev=None):
         if ev:
             ev[0].record()
-        _lib.check(L.hf_fill_masked(n, dv.ptr(y), dv.ptr(x), mask, 0.0, dv.stream()))
+        local_op.apply_into(x, y)
         if ev:
             ev[1].record()
-        local_op.apply_raw(x, y)
-        if ev:
-            ev[2].record()
         if exchange is not None:
             exchange.add(y)
         if ev:
-            ev[3].record()
+            ev[2].record()
 
     for _ in range(warmup):
         if flush_l2:
             flush.zero_()
         one()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
     for k in range(steps):
         if flush_l2:
             flush.zero_()
         one(evs[k])
     torch.cuda.synchronize()
-    step = [e[0].elapsed_time(e[3]) for e in evs]
-    kern = [e[1].elapsed_time(e[2]) for e in evs]
-    launches = 2 + (len(exchange.peers) if exchange is not None else 0)
+    step = [e[0].elapsed_time(e[2]) for e in evs]
+    kern = [e[0].elapsed_time(e[1]) for e in evs]
+    launches = 1 + (len(exchange.peers) if exchange is not None else 0)
     return float(np.mean(step)), float(np.mean(kern)), launches
 
 

@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -377,8 +378,8 @@ HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev,
   return HF_OK;
 }
 
-HF_API int hf_tangent_apply_raw(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
-                                void* stream) {
+static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev, int fill,
+                         void* stream) {
   if (!op || !x_dev || !y_dev) return fail(HF_ERR_ARG, "null argument");
   CellArgs a = base_args(op->sp);
   a.x = x_dev;
@@ -386,18 +387,31 @@ HF_API int hf_tangent_apply_raw(hf_tangent* op, const double* x_dev, double* y_d
   a.cache = op->d_cache;
   a.ubar = op->d_ubar;
   a.skip = skip_dev;
+  a.fill = fill;
   HF_CUDA(cell(op->sp, OP_APPLY, op->strategy, a, S(stream)));
   return HF_OK;
 }
 
+HF_API int hf_tangent_apply_raw(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                void* stream) {
+  return tangent_apply(op, x_dev, y_dev, skip_dev, 0, stream);
+}
+
+// y = mask ? x : 0, then the cell kernel as its programmatic dependent
+// launch: the apply overlaps the fill and waits for it only before scattering
 HF_API int hf_tangent_apply_flagged(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
                                     void* stream) {
   if (!op || !x_dev || !y_dev) return fail(HF_ERR_ARG, "null argument");
-  const hf_space* sp = op->sp;
-  cudaStream_t s = S(stream);
-  k_fill_masked<<<vec_blocks(sp->n_dofs), 256, 0, s>>>(sp->n_dofs, y_dev, x_dev, sp->d_mask, 0.0, skip_dev);
+  static int pdl = -1;
+  if (pdl < 0) {
+    const char* e = std::getenv("HF_PDL");
+    pdl = e ? std::atoi(e) : 1;
+  }
+  k_fill_masked<<<vec_blocks(op->sp->n_dofs), 256, 0, S(stream)>>>(op->sp->n_dofs, y_dev, x_dev, op->sp->d_mask, 0.0,
+                                                                   skip_dev);
   HF_CUDA(cudaGetLastError());
-  return hf_tangent_apply_raw(op, x_dev, y_dev, skip_dev, stream);
+  if (op->sp->lat.n_el == 0) return HF_OK;
+  return tangent_apply(op, x_dev, y_dev, skip_dev, pdl, stream);
 }
 
 HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream) {

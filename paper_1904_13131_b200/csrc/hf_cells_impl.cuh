@@ -36,6 +36,7 @@ cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
   a.mask = c.mask;
   a.lmask = c.lmask;
   a.skip = c.skip;
+  a.fill = c.fill;
   TabLine<N> T;
   for (int l = 0; l < N; ++l)
     for (int o = 0; o < N; ++o) {
@@ -46,8 +47,22 @@ cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
   long long nb = (tiles + PL::W - 1) / PL::W;
   if (nb > resident) nb = resident;
   if (nb <= 0) return cudaSuccess;
-  k_apply_line<DIM, N, VAR><<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);
-  return cudaGetLastError();
+  if (!c.fill) {
+    k_apply_line<DIM, N, VAR><<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);
+    return cudaGetLastError();
+  }
+  // programmatic dependent launch after the fill kernel (hf_api.cu)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nb);
+  cfg.blockDim = dim3(PL::NT);
+  cfg.dynamicSmemBytes = PL::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_apply_line<DIM, N, VAR>, a, T);
 }
 
 template <int DIM, int N>

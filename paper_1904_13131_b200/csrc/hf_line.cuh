@@ -64,6 +64,7 @@ struct LineArgs {
   const uint8_t* mask;
   const uint32_t* lmask;  // constraint bits per (cell, last-axis line)
   const int* skip;
+  int fill;  // launched as the PDL secondary of the y = mask ? x : 0 fill (operators.py:333-338)
 };
 
 // Per-warp line-buffer layout: element (cell m, component c, point i,j,k) at
@@ -337,6 +338,11 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
     for (int j = 0; j < RW; ++j) issue(j);
   }
   __syncwarp();
+  // y = mask ? x : 0 is written by the preceding k_fill_masked launch.  With
+  // programmatic dependent launch (a.fill != 0) this kernel starts while that
+  // fill is still running: TMA loads, gathers and the evaluation overlap it,
+  // and griddepcontrol.wait orders only the first scatter-add after it.
+  bool synced = !a.fill;
 
   const int m = lane / K::L;
   const int t = lane - m * K::L;
@@ -522,6 +528,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
       __syncwarp();
     }
     // ---------------- I4: last axis, scatter-add ----------------
+    if (!synced) {  // the fill kernel (PDL primary) has completed and its writes are visible
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      synced = true;
+    }
     if (live) {
       double v[DIM][N];
       ld_line<DIM, N, DIM - 1>(Q, t, v);

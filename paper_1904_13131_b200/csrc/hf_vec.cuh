@@ -92,6 +92,7 @@ __global__ void k_dot(long long n, const double* __restrict__ a, const double* _
 // y[i] = mask[i] ? (x ? x[i] : mval) : 0
 __global__ void k_fill_masked(long long n, double* __restrict__ y, const double* __restrict__ x,
                               const uint8_t* __restrict__ mask, double mval, const int* skip) {
+  asm volatile("griddepcontrol.launch_dependents;");  // a PDL secondary (the apply) may start now
   if (skip && *skip) return;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     y[i] = mask[i] ? (x ? x[i] : mval) : 0.0;
