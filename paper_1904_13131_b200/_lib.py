@@ -8,7 +8,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhf.so")
+LIB_PATH = os.environ.get("HF_LIB") or os.path.join(_HERE, "libhf.so")  # HF_LIB: A/B builds only
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "hf.h")
 
 HF_OK, HF_ERR_ARG, HF_ERR_CUDA, HF_ERR_UNSUPPORTED, HF_ERR_JACOBIAN, HF_ERR_GEOMETRY = 0, 1, 2, 3, 4, 5

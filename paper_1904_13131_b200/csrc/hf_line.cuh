@@ -298,7 +298,10 @@ struct LinePlan {
   // tile of stages would cost 3 of 7 resident warps, so the ring stays 3 deep.
   static constexpr int RW = N < 3 ? N : 3;
   static constexpr int W0 = (int)(BUDGET / perw(RW));
-  static constexpr int W = W0 > 8 ? 8 : (W0 < 1 ? 1 : W0);
+  // warps per block: shared memory bound, capped so the registers of the
+  // heaviest variant still fit (scalar ~210 regs -> 8 warps, others ~170 -> 12)
+  static constexpr int WMAX = VAR == SCALAR ? 8 : 12;
+  static constexpr int W = W0 > WMAX ? WMAX : (W0 < 1 ? 1 : W0);
   static constexpr int NT = 32 * W;
   static constexpr size_t SMEM = (size_t)W * perw(RW);
 };
@@ -383,102 +386,121 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
       lam = __ldg(a.lam + e);
     }
     const int pt0 = lbase<DIM, N, 0>(t);
-#pragma unroll
-    for (int iq = 0; iq < N; ++iq, ++jc) {
-      const int s = (int)(jc % RW);
-      mbar_wait(full + s, (unsigned)((jc / RW) & 1));
-      const double* st = ring + (size_t)s * CH + lane;
+    // one Gauss point of this thread's x-line from its cache chunk
+    auto point = [&](const int iq, const double* st) {
       if (live) {
-        const int pt = pt0 + iq;
-        double f[NF];
+      const int pt = pt0 + iq;
+      double f[NF];
 #pragma unroll
-        for (int q = 0; q < NF; ++q) f[q] = st[q * K::LANES];
-        double gu[DIM][DIM];
+      for (int q = 0; q < NF; ++q) f[q] = st[q * K::LANES];
+      double gu[DIM][DIM];
 #pragma unroll
-        for (int cc = 0; cc < DIM; ++cc) {
-          gu[cc][0] = Gx[cc][iq];
-          gu[cc][1] = G1[(cc * Y::NP + pt) * Y::CPWP];
-          if (DIM == 3) gu[cc][DIM - 1] = G2[(cc * Y::NP + pt) * Y::CPWP];
-        }
-        double G[DIM][DIM];
-        if (VAR == TENSOR4) {
-          double sinv[DIM][DIM], tau[DIM][DIM];
-#pragma unroll
-          for (int i = 0; i < DIM; ++i)
-#pragma unroll
-            for (int j = 0; j < DIM; ++j) {
-              tau[i][j] = f[hf_slot<DIM>(i, j)];
-              sinv[i][j] = f[NV + NM + i * DIM + j];
-            }
-          qp_action<DIM, true>(gu, sinv, tau, 0.0, 0.0, f + NV, f[NF - 1], G);
-        } else if (VAR == TENSOR2) {
-          double sinv[DIM][DIM], tau[DIM][DIM];
-#pragma unroll
-          for (int i = 0; i < DIM; ++i)
-#pragma unroll
-            for (int j = 0; j < DIM; ++j) {
-              tau[i][j] = f[2 + hf_slot<DIM>(i, j)];
-              sinv[i][j] = f[2 + NV + i * DIM + j];
-            }
-          qp_action<DIM, false>(gu, sinv, tau, f[0], f[1], nullptr, f[NF - 1], G);
-        } else {
-          // rebuild F, b, tau = mu b - c1 I and s_inv from ubar (operators.py:349-363)
-          double ji[DIM][DIM];
-#pragma unroll
-          for (int r = 0; r < DIM; ++r)
-#pragma unroll
-            for (int q = 0; q < DIM; ++q) ji[r][q] = f[1 + r * DIM + q];
-          double gub[DIM][DIM];
-#pragma unroll
-          for (int cc = 0; cc < DIM; ++cc) {
-            gub[cc][0] = Gxu[cc][iq];
-            gub[cc][1] = bufs[3][(cc * Y::NP + pt) * Y::CPWP];
-            if (DIM == 3) gub[cc][DIM - 1] = bufs[4][(cc * Y::NP + pt) * Y::CPWP];
-          }
-          double F[DIM * DIM];
-#pragma unroll
-          for (int i = 0; i < DIM; ++i)
-#pragma unroll
-            for (int Aa = 0; Aa < DIM; ++Aa) {
-              double sm = (i == Aa) ? 1.0 : 0.0;
-#pragma unroll
-              for (int q = 0; q < DIM; ++q) sm = fma(gub[i][q], ji[q][Aa], sm);
-              F[i * DIM + Aa] = sm;
-            }
-          const double c1 = f[0];
-          double tau[DIM][DIM], sinv[DIM][DIM], Fi[DIM * DIM];
-#pragma unroll
-          for (int i = 0; i < DIM; ++i)
-#pragma unroll
-            for (int j = 0; j < DIM; ++j) {
-              double bb = 0.0;
-#pragma unroll
-              for (int Aa = 0; Aa < DIM; ++Aa) bb = fma(F[i * DIM + Aa], F[j * DIM + Aa], bb);
-              tau[i][j] = mu * bb - (i == j ? c1 : 0.0);
-            }
-          hf_inv<DIM>(F, hf_det<DIM>(F), Fi);
-#pragma unroll
-          for (int q = 0; q < DIM; ++q)
-#pragma unroll
-            for (int j = 0; j < DIM; ++j) {
-              double sm = 0.0;
-#pragma unroll
-              for (int Aa = 0; Aa < DIM; ++Aa) sm = fma(ji[q][Aa], Fi[Aa * DIM + j], sm);
-              sinv[q][j] = sm;
-            }
-          qp_action<DIM, false>(gu, sinv, tau, 2.0 * c1, 2.0 * lam, nullptr, f[NF - 1], G);
-        }
-#pragma unroll
-        for (int cc = 0; cc < DIM; ++cc) {
-          Q[(cc * Y::NP + pt) * Y::CPWP] = G[cc][0];
-          G1[(cc * Y::NP + pt) * Y::CPWP] = G[cc][1];
-          if (DIM == 3) G2[(cc * Y::NP + pt) * Y::CPWP] = G[cc][DIM - 1];
-        }
+      for (int cc = 0; cc < DIM; ++cc) {
+        gu[cc][0] = Gx[cc][iq];
+        gu[cc][1] = G1[(cc * Y::NP + pt) * Y::CPWP];
+        if (DIM == 3) gu[cc][DIM - 1] = G2[(cc * Y::NP + pt) * Y::CPWP];
       }
+      double G[DIM][DIM];
+      if (VAR == TENSOR4) {
+        double sinv[DIM][DIM], tau[DIM][DIM];
+#pragma unroll
+        for (int i = 0; i < DIM; ++i)
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) {
+            tau[i][j] = f[hf_slot<DIM>(i, j)];
+            sinv[i][j] = f[NV + NM + i * DIM + j];
+          }
+        qp_action<DIM, true>(gu, sinv, tau, 0.0, 0.0, f + NV, f[NF - 1], G);
+      } else if (VAR == TENSOR2) {
+        double sinv[DIM][DIM], tau[DIM][DIM];
+#pragma unroll
+        for (int i = 0; i < DIM; ++i)
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) {
+            tau[i][j] = f[2 + hf_slot<DIM>(i, j)];
+            sinv[i][j] = f[2 + NV + i * DIM + j];
+          }
+        qp_action<DIM, false>(gu, sinv, tau, f[0], f[1], nullptr, f[NF - 1], G);
+      } else {
+        // rebuild F, b, tau = mu b - c1 I and s_inv from ubar (operators.py:349-363)
+        double ji[DIM][DIM];
+#pragma unroll
+        for (int r = 0; r < DIM; ++r)
+#pragma unroll
+          for (int q = 0; q < DIM; ++q) ji[r][q] = f[1 + r * DIM + q];
+        double gub[DIM][DIM];
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc) {
+          gub[cc][0] = Gxu[cc][iq];
+          gub[cc][1] = bufs[3][(cc * Y::NP + pt) * Y::CPWP];
+          if (DIM == 3) gub[cc][DIM - 1] = bufs[4][(cc * Y::NP + pt) * Y::CPWP];
+        }
+        double F[DIM * DIM];
+#pragma unroll
+        for (int i = 0; i < DIM; ++i)
+#pragma unroll
+          for (int Aa = 0; Aa < DIM; ++Aa) {
+            double sm = (i == Aa) ? 1.0 : 0.0;
+#pragma unroll
+            for (int q = 0; q < DIM; ++q) sm = fma(gub[i][q], ji[q][Aa], sm);
+            F[i * DIM + Aa] = sm;
+          }
+        const double c1 = f[0];
+        double tau[DIM][DIM], sinv[DIM][DIM], Fi[DIM * DIM];
+#pragma unroll
+        for (int i = 0; i < DIM; ++i)
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) {
+            double bb = 0.0;
+#pragma unroll
+            for (int Aa = 0; Aa < DIM; ++Aa) bb = fma(F[i * DIM + Aa], F[j * DIM + Aa], bb);
+            tau[i][j] = mu * bb - (i == j ? c1 : 0.0);
+          }
+        hf_inv<DIM>(F, hf_det<DIM>(F), Fi);
+#pragma unroll
+        for (int q = 0; q < DIM; ++q)
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) {
+            double sm = 0.0;
+#pragma unroll
+            for (int Aa = 0; Aa < DIM; ++Aa) sm = fma(ji[q][Aa], Fi[Aa * DIM + j], sm);
+            sinv[q][j] = sm;
+          }
+        qp_action<DIM, false>(gu, sinv, tau, 2.0 * c1, 2.0 * lam, nullptr, f[NF - 1], G);
+      }
+#pragma unroll
+      for (int cc = 0; cc < DIM; ++cc) {
+        Q[(cc * Y::NP + pt) * Y::CPWP] = G[cc][0];
+        G1[(cc * Y::NP + pt) * Y::CPWP] = G[cc][1];
+        if (DIM == 3) G2[(cc * Y::NP + pt) * Y::CPWP] = G[cc][DIM - 1];
+      }
+    }
+    };
+    if constexpr (RW >= N) {
+      // the whole tile's chunks are resident: wait once, then the N points
+      // are free of barriers and the compiler interleaves their chains
+#pragma unroll
+      for (int iq = 0; iq < N; ++iq) mbar_wait(full + (int)((jc + iq) % RW), (unsigned)(((jc + iq) / RW) & 1));
+#pragma unroll
+      for (int iq = 0; iq < N; ++iq) point(iq, ring + (size_t)((jc + iq) % RW) * CH + lane);
       __syncwarp();
-      if (lane == 0) {  // stage consumed by every lane: refill it with chunk jc + RW
+      if (lane == 0) {  // stages consumed by every lane: refill them with the next tile's chunks
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(jc + RW);
+#pragma unroll 1
+        for (int iq = 0; iq < N; ++iq) issue(jc + iq + RW);
+      }
+      jc += N;
+    } else {
+#pragma unroll
+      for (int iq = 0; iq < N; ++iq, ++jc) {
+        const int s = (int)(jc % RW);
+        mbar_wait(full + s, (unsigned)((jc / RW) & 1));
+        point(iq, ring + (size_t)s * CH + lane);
+        __syncwarp();
+        if (lane == 0) {  // stage consumed by every lane: refill it with chunk jc + RW
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(jc + RW);
+        }
       }
     }
     __syncwarp();
