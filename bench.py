@@ -270,8 +270,15 @@ def run_ours(args):
     if ws > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # HF_BENCH_BACKEND=gloo runs the N>1 code path with every rank on one
+        # GPU (exchange staged through the host) -- a functional check only
+        backend = os.environ.get("HF_BENCH_BACKEND", "nccl")
+        dev = local % torch.cuda.device_count()
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     from paper_1904_13131_b200 import MatrixFreeTangent
@@ -338,6 +345,16 @@ def run_ours(args):
             "gpu_launches": launches * args.steps, "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_extra:
         line.update(_extras(args, hbm, prob, ubar, x, y, flush, nqp))
+    if not args.no_extra:
+        from paper_1904_13131_b200.distributed import LocalComm
+
+        del op, x, y
+        if public is not None:
+            del public
+        comm5 = TorchComm() if ws > 1 else LocalComm()
+        line["cfg5_strong"] = _cfg5(comm5, 10, 3)
+        if ws > 1 and not args.no_newton:
+            line["newton_slabs"] = _dist_newton(comm5)
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, dt, n, _ = cpu_baseline(2, "tensor4", budget_s=20.0, threads=1)
         line["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": 1, "kind": "port",
@@ -378,6 +395,101 @@ def _extras(args, hbm, prob, ubar, x, y, flush, nqp):
     if not args.no_newton:
         out["newton"] = _newton_iteration()
     return out
+
+
+def _cfg5(comm, steps: int, warmup: int):
+    """Config 5 (128^3 Q2, 50.9M DoFs, 1280 inclusions): tangent vmult and a
+    10-iteration GMG-CG on the slab decomposition over all ranks (strong
+    scaling: the global problem is fixed), NCCL interface exchange and dot
+    all-reduce timed separately (device events).  Amplitude 0.005 (SPD, H4)."""
+    import torch
+
+    from paper_1904_13131_b200.distributed import CommTimer, build_dist_gmg, dist_cg, level_slabs
+    from paper_1904_13131_b200.workloads import AMP_SOLVE, MATERIAL, host_workload
+
+    t_setup = time.perf_counter()
+    hw = host_workload(5, seed=0, amp=AMP_SOLVE, levels=True)
+    fine = hw.meshes[-1]
+    sl = level_slabs(3, 2, fine.cells, len(hw.meshes), comm.rank, comm.size)[-1]
+    gmg, dp, op = build_dist_gmg(hw.meshes, 2, MATERIAL, hw.masks, np.ascontiguousarray(sl.local(hw.ubar)), comm)
+    x = torch.from_numpy(np.ascontiguousarray(sl.local(hw.x))).cuda()
+    y = torch.empty_like(x)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    timer = CommTimer()
+    for lv in gmg.levels:
+        lv.dp.set_timer(timer)
+    for _ in range(warmup):
+        op.apply_into(x, y)
+    torch.cuda.synchronize()
+    timer.reset()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        op.apply_into(x, y)
+    e1.record()
+    torch.cuda.synchronize()
+    vm_ms = e0.elapsed_time(e1) / steps
+    vm_comm = timer.totals_ms()
+    b = y.clone()
+    b[dp.mask_dev.bool()] = 0.0
+    dist_cg(dp, op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=2)  # warm-up (graph capture)
+    torch.cuda.synchronize()
+    timer.reset()
+    e0.record()
+    _, its, relres, _ = dist_cg(dp, op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=10)
+    e1.record()
+    torch.cuda.synchronize()
+    cg_ms = e0.elapsed_time(e1)
+    cg_comm = timer.totals_ms()
+    t = torch.tensor([vm_ms, cg_ms, vm_comm["exchange"] / steps, cg_comm["exchange"], cg_comm["allreduce"]],
+                     dtype=torch.float64, device="cuda")
+    if comm.size > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    vm_ms, cg_ms, vx, cx, ca = t.tolist()
+    n = sl.n_global_dofs
+    return {"workload": "cfg5 128^3 Q2 (50,923,779 DoFs), levels 4..128, strong scaling over slabs",
+            "n_gpus": comm.size, "setup_s": t_setup, "vmult_ms": vm_ms, "vmult_GDoF_s": n / vm_ms / 1e6,
+            "vmult_exchange_ms": vx, "cg10_ms": cg_ms, "cg_iterations": its, "cg_relres_after_10": relres,
+            "cg10_exchange_ms": cx, "cg10_allreduce_ms": ca, "cg10_n_allreduce": cg_comm["n_allreduce"]}
+
+
+def _dist_newton(comm):
+    """First Newton iteration of load step 1 of config 4 on the slab
+    decomposition (tangent + distributed GMG build, CG to 1e-6, residual)."""
+    import torch
+
+    from paper_1904_13131_b200.distributed import build_dist_gmg, dist_cg, level_slabs
+    from paper_1904_13131_b200.workloads import MATERIAL, host_workload
+    from paper_1904_13131_b200.fespace import build_dof_map, node_coordinates
+
+    hw = host_workload(4, seed=0, levels=True, with_x=False)
+    fine = hw.meshes[-1]
+    sl = level_slabs(3, 2, fine.cells, len(hw.meshes), comm.rank, comm.size)[-1]
+    X = node_coordinates(fine, build_dof_map(fine, 2, 3))
+    ug = np.zeros(X.shape[0] * 3)
+    ug.reshape(-1, 3)[:, 2] = (-0.05 / 5) * X[:, 2] / X[:, 2].max()
+    rec = None
+    for _ in range(2):
+        u = torch.from_numpy(np.ascontiguousarray(sl.local(ug))).cuda()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gmg, dp, op = build_dist_gmg(hw.meshes, 2, MATERIAL, hw.masks, u, comm, keep_constrained=True)
+        res = dp.residual(u)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        du, its, relres, _ = dist_cg(dp, op, -res, rel_tol=1e-6, preconditioner=gmg)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        u += du
+        res = dp.residual(u)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        rec = {"workload": "cfg4 64^3 Q2 levels 4..64, load step 1, Newton iteration 1 (slab decomposition)",
+               "n_gpus": comm.size, "newton_iteration_s": t3 - t0, "setup_s": t1 - t0, "cg_s": t2 - t1,
+               "cg_iterations": its, "note": "setup includes the host-side slab problem construction"}
+        del gmg, dp, op
+    return rec
 
 
 def _newton_iteration():

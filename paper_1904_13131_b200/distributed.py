@@ -110,6 +110,56 @@ class TorchComm:
         self.dist.barrier(group=self.group)
 
 
+class CommTimer:
+    """Optional device-side timing of the collectives (config 5 reports the
+    interface exchange and the dot-product all-reduce separately): CUDA event
+    pairs on the current stream, summed when read."""
+
+    def __init__(self):
+        self.events = {"exchange": [], "allreduce": []}
+
+    def span(self, kind: str):
+        timer = self
+
+        class _Span:
+            def __enter__(self_):
+                self_.e0 = torch.cuda.Event(enable_timing=True)
+                self_.e1 = torch.cuda.Event(enable_timing=True)
+                self_.e0.record()
+
+            def __exit__(self_, *a):
+                self_.e1.record()
+                timer.events[kind].append((self_.e0, self_.e1))
+
+        return _Span()
+
+    def totals_ms(self) -> dict:
+        torch.cuda.synchronize()
+        return {k: float(sum(a.elapsed_time(b) for a, b in v)) for k, v in self.events.items()} | \
+            {f"n_{k}": len(v) for k, v in self.events.items()}
+
+    def reset(self):
+        for v in self.events.values():
+            v.clear()
+
+
+class _NoTimer:
+    def span(self, kind):
+        return _NULL
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+_NULL = _Null()
+NO_TIMER = _NoTimer()
+
+
 # ---------------------------------------------------------------------------
 # partition
 # ---------------------------------------------------------------------------
@@ -227,6 +277,7 @@ class SlabExchange:
 
     def __init__(self, slab: Slab, comm, mask_dev: torch.Tensor, add_fn=_halo_add_dev):
         self.slab, self.comm, self.add_fn = slab, comm, add_fn
+        self.timer = NO_TIMER
         pd = slab.plane_dofs
         self.pd = pd
         self.peers = {}
@@ -240,10 +291,11 @@ class SlabExchange:
     def add(self, y: torch.Tensor) -> torch.Tensor:
         if not self.peers:
             return y
-        sends = {p: y[s].contiguous() for p, s in self.peers.items()}
-        self.comm.exchange(sends, self.recv)
-        for p, s in self.peers.items():
-            self.add_fn(y[s], self.recv[p], self.mask[p])
+        with self.timer.span("exchange"):
+            sends = {p: y[s].contiguous() for p, s in self.peers.items()}
+            self.comm.exchange(sends, self.recv)
+            for p, s in self.peers.items():
+                self.add_fn(y[s], self.recv[p], self.mask[p])
         return y
 
 
@@ -260,6 +312,11 @@ class DistProblem:
         self.local.constraints = ConstraintSet.from_dofs(self.local.n_dofs, np.flatnonzero(mask))
         self.mask_dev = torch.from_numpy(mask.astype(np.uint8)).cuda()
         self.exchange = SlabExchange(slab, comm, self.mask_dev)
+        self.timer = NO_TIMER
+
+    def set_timer(self, timer) -> None:
+        self.timer = timer
+        self.exchange.timer = timer
 
     @property
     def n_dofs(self) -> int:
@@ -273,7 +330,8 @@ class DistProblem:
         """Global dot product: owned DoFs on this rank, all-reduced (2 scalars max per call site)."""
         o = self.slab.owned
         dv.dot(a[o], b[o], out)
-        return self.comm.allreduce_(out)
+        with self.timer.span("allreduce"):
+            return self.comm.allreduce_(out)
 
     def residual(self, u: torch.Tensor, traction=None) -> torch.Tensor:
         """compute_residual (operators.py:205-224) on the slab + interface add."""
