@@ -1,0 +1,78 @@
+"""Parity at the BASELINE sizes: the CPU oracle is run where it
+finishes in seconds (config 1 2D 32^2 Q2, 3D 16^3 Q2), and size-independent
+properties are checked at configs 2 and 3 (823,875 DoFs): the three caching
+strategies agree, the operator is symmetric and linear, and it is the identity
+on the constrained subspace (operators.py:331-339)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hf_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _oracle_of(p):
+    inc = p.mesh.material_id == 1
+    from paper_1904_13131_b200.workloads import MATERIAL
+
+    mu = np.where(inc, MATERIAL.inclusion.mu, MATERIAL.matrix.mu)
+    lam = np.where(inc, MATERIAL.inclusion.lam, MATERIAL.matrix.lam)
+    return O.OProblem(p.dim, p.degree, p.mesh.cells, p.mesh.vertices, mu, lam, p.constraints.mask)
+
+
+def _rel(a, b):
+    return float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+
+
+@pytest.mark.parametrize("cfg,m", [(1, None), (2, 16)])
+def test_apply_diagonal_residual_vs_oracle_at_size(cfg, m):
+    from paper_1904_13131_b200 import MatrixFreeTangent, compute_residual
+    from paper_1904_13131_b200.workloads import make_workload
+
+    wl = make_workload(cfg, seed=5, m=m)
+    p = wl.fine
+    op_ = _oracle_of(p)
+    for s in ("scalar", "tensor2", "tensor4"):
+        y = MatrixFreeTangent(p, wl.ubar, s).apply(wl.x)
+        yo = O.Tangent(op_, wl.ubar, s).apply(wl.x)
+        assert np.linalg.norm(y - yo) / np.linalg.norm(yo) < TOL, s
+    r = compute_residual(p, wl.ubar)
+    ro = O.residual(op_, wl.ubar)
+    assert np.linalg.norm(r - ro) / np.linalg.norm(ro) < TOL
+    if cfg == 1:
+        d = MatrixFreeTangent(p, wl.ubar, "tensor4").diagonal().cpu().numpy()
+        do = O.Tangent(op_, wl.ubar, "tensor4").diagonal()
+        assert np.linalg.norm(d - do) / np.linalg.norm(do) < TOL
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_properties_at_full_size(cfg):
+    from paper_1904_13131_b200 import MatrixFreeTangent
+    from paper_1904_13131_b200.workloads import make_workload
+
+    wl = make_workload(cfg, seed=0)
+    p = wl.fine
+    x = torch.from_numpy(wl.x).cuda()
+    z = torch.from_numpy(np.random.default_rng(9).standard_normal(p.n_dofs)).cuda()
+    mask = p.mask_dev
+    ys = {}
+    for s in ("tensor4", "tensor2", "scalar"):
+        op = MatrixFreeTangent(p, wl.ubar, s)
+        ys[s] = op.apply(x)
+        if s == "tensor4":
+            az = op.apply(z)
+            # symmetric: <Ax, z> = <x, Az>
+            lhs, rhs = float(ys[s] @ z), float(x @ az)
+            assert abs(lhs - rhs) <= 1e-12 * float(torch.linalg.norm(ys[s]) * torch.linalg.norm(z))
+            # linear
+            a, b = 0.7, -1.3
+            assert _rel(op.apply(a * x + b * z), a * ys[s] + b * az) < TOL
+            # identity on the constrained subspace, exactly; atomics reorder sums only
+            assert torch.equal(ys[s][mask], x[mask])
+            assert _rel(op.apply(x), ys[s]) < 1e-14
+            assert op.storage_bytes() == 8 * p.mesh.n_elements * p.n_qpoints_per_cell * (6 + 21 + 9 + 1)
+    assert _rel(ys["tensor2"], ys["tensor4"]) < TOL
+    assert _rel(ys["scalar"], ys["tensor4"]) < TOL
