@@ -100,6 +100,10 @@ HF_API int hf_tangent_apply_flagged(hf_tangent* op, const double* x_dev, double*
  * (_local_apply + distribute_local_to_global, 341-393 / fespace.py:307-324) */
 HF_API int hf_tangent_apply_raw(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
                                 void* stream);
+/* the cell kernel of .apply only, when the previous kernel on the stream
+ * wrote x and y = mask ? x : 0 (hf_cheb_step_fill); programmatic dependent launch */
+HF_API int hf_tangent_apply_after_fill(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                       void* stream);
 /* .diagonal (395-410) */
 HF_API int hf_tangent_diagonal(hf_tangent* op, double* diag_dev, void* stream);
 /* .storage_bytes (412-417), cache.payload_scalars_per_qpoint / payload_nbytes (244-289) */
@@ -143,6 +147,12 @@ HF_API int hf_fill_masked(long long n, double* y, const double* x, const unsigne
  * (ax == NULL means A x = 0) */
 HF_API int hf_cheb_step(long long n, double* x, double* d, const double* b, const double* ax, const double* inv_d,
                         int first, double theta, double cd, double cz, int x_zero, const int* skip_dev, void* stream);
+/* hf_cheb_step + the initialisation y_next = mask ? x_new : 0 of the next
+ * tangent apply, which is then launched with hf_tangent_apply_after_fill as
+ * this kernel's programmatic dependent (y_next may alias ax) */
+HF_API int hf_cheb_step_fill(long long n, double* x, double* d, const double* b, const double* ax, const double* inv_d,
+                             int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
+                             const unsigned char* mask, double* y_next, void* stream);
 /* r = b - ax; r[mask] = 0 (v_cycle, multigrid.py:324-325) */
 HF_API int hf_resid_masked(long long n, double* r, const double* b, const double* ax, const unsigned char* mask,
                            void* stream);

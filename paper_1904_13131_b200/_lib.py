@@ -47,6 +47,7 @@ _SIGS = {
     "hf_tangent_apply": (I, [P, P, P, P]),
     "hf_tangent_apply_flagged": (I, [P, P, P, P, P]),
     "hf_tangent_apply_raw": (I, [P, P, P, P, P]),
+    "hf_tangent_apply_after_fill": (I, [P, P, P, P, P]),
     "hf_tangent_diagonal": (I, [P, P, P]),
     "hf_tangent_storage": (I, [P, ct.POINTER(LL), ct.POINTER(I), ct.POINTER(LL)]),
     "hf_tangent_destroy": (I, [P]),
@@ -61,6 +62,7 @@ _SIGS = {
     "hf_dot": (I, [P, LL, P, P, P, P, P]),
     "hf_fill_masked": (I, [LL, P, P, P, D, P]),
     "hf_cheb_step": (I, [LL, P, P, P, P, P, I, D, D, D, I, P, P]),
+    "hf_cheb_step_fill": (I, [LL, P, P, P, P, P, I, D, D, D, I, P, P, P, P]),
     "hf_resid_masked": (I, [LL, P, P, P, P, P]),
     "hf_resnorm_check": (I, [P, LL, P, P, P, I, I, P, P]),
     "hf_scalar_op": (I, [I, P, I, I, D, P, P]),

@@ -414,6 +414,14 @@ HF_API int hf_tangent_apply_flagged(hf_tangent* op, const double* x_dev, double*
   return tangent_apply(op, x_dev, y_dev, skip_dev, pdl, stream);
 }
 
+// the cell kernel alone, as the programmatic dependent of a kernel that has
+// written both x and y = mask ? x : 0 (hf_cheb_step_fill)
+HF_API int hf_tangent_apply_after_fill(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                       void* stream) {
+  if (op && op->sp->lat.n_el == 0) return HF_OK;
+  return tangent_apply(op, x_dev, y_dev, skip_dev, 2, stream);
+}
+
 HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream) {
   return hf_tangent_apply_flagged(op, x_dev, y_dev, nullptr, stream);
 }
@@ -653,7 +661,18 @@ HF_API int hf_cheb_step(long long n, double* x, double* d, const double* b, cons
                         int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
                         void* stream) {
   if (!x || !d || !b || !inv_d) return fail(HF_ERR_ARG, "null argument");
-  k_cheb<<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev);
+  k_cheb<<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev,
+                                               nullptr, nullptr);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_cheb_step_fill(long long n, double* x, double* d, const double* b, const double* ax, const double* inv_d,
+                             int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
+                             const unsigned char* mask, double* y_next, void* stream) {
+  if (!x || !d || !b || !inv_d || !mask || !y_next) return fail(HF_ERR_ARG, "null argument");
+  k_cheb<<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev, mask,
+                                               y_next);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }

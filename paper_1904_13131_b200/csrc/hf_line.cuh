@@ -64,7 +64,10 @@ struct LineArgs {
   const uint8_t* mask;
   const uint32_t* lmask;  // constraint bits per (cell, last-axis line)
   const int* skip;
-  int fill;  // launched as the PDL secondary of the y = mask ? x : 0 fill (operators.py:333-338)
+  // 0: plain launch (y already initialised by an earlier kernel)
+  // 1: PDL secondary of the y = mask ? x : 0 fill (operators.py:333-338): wait before the first scatter
+  // 2: PDL secondary of a kernel that wrote x and y (hf_cheb_step_fill): wait before the first gather
+  int fill;
 };
 
 // Per-warp line-buffer layout: element (cell m, component c, point i,j,k) at
@@ -345,7 +348,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
   // programmatic dependent launch (a.fill != 0) this kernel starts while that
   // fill is still running: TMA loads, gathers and the evaluation overlap it,
   // and griddepcontrol.wait orders only the first scatter-add after it.
-  bool synced = !a.fill;
+  bool synced = a.fill != 1;
+  if (a.fill == 2) asm volatile("griddepcontrol.wait;" ::: "memory");  // x comes from the primary
 
   const int m = lane / K::L;
   const int t = lane - m * K::L;

@@ -102,15 +102,22 @@ __global__ void k_fill_masked(long long n, double* __restrict__ y, const double*
 //   z = inv_d * (b - ax)        (ax == nullptr -> A x = 0)
 //   first:  d = z / theta       else d = cd * d + cz * z
 //   x = (x_zero ? 0 : x) + d
+//   fill_mask != null: also y_next = mask ? x_new : 0, the initialisation of
+//   the NEXT tangent apply (which is launched as this kernel's programmatic
+//   dependent and skips its own fill); y_next may alias ax (read first)
 __global__ void k_cheb(long long n, double* __restrict__ x, double* __restrict__ d, const double* __restrict__ b,
-                       const double* __restrict__ ax, const double* __restrict__ inv_d, int first, double theta,
-                       double cd, double cz, int x_zero, const int* skip) {
+                       const double* ax, const double* __restrict__ inv_d, int first, double theta, double cd,
+                       double cz, int x_zero, const int* skip, const uint8_t* __restrict__ fill_mask,
+                       double* y_next) {
+  asm volatile("griddepcontrol.launch_dependents;");
   if (skip && *skip) return;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     double z = inv_d[i] * (b[i] - (ax ? ax[i] : 0.0));
     double di = first ? z / theta : cd * d[i] + cz * z;
     d[i] = di;
-    x[i] = x_zero ? di : x[i] + di;
+    const double xn = x_zero ? di : x[i] + di;
+    x[i] = xn;
+    if (fill_mask) y_next[i] = fill_mask[i] ? xn : 0.0;
   }
 }
 

@@ -199,22 +199,50 @@ def _cheb_coeffs(lam_max: float, s: ChebyshevSettings):
     return theta, coefs
 
 
-def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings, steps: int, x_zero: bool):
-    """In-place restarted Chebyshev on device buffers (multigrid.py:176-205)."""
+def _apply_maybe_filled(apply_fn, x, ax, prefilled: bool, skip=None):
+    if prefilled:
+        return apply_fn.apply_after_fill(x, ax, skip)
+    return _apply_into(apply_fn, x, ax, skip)
+
+
+def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings, steps: int, x_zero: bool,
+                    mask=None, fill_last: bool = False):
+    """In-place restarted Chebyshev on device buffers (multigrid.py:176-205).
+
+    With ``mask`` (and an operator that has ``apply_after_fill``), every
+    Chebyshev update also writes ax = mask ? x : 0 for the next operator
+    application, which then runs as its programmatic dependent launch;
+    ``fill_last`` does so after the final update too (the V-cycle's residual
+    apply follows the pre-smoother)."""
     theta, coefs = _cheb_coeffs(lam_max, s)
     n = x.numel()
     L = lib()
+    fuse = mask is not None and hasattr(apply_fn, "apply_after_fill")
+    filled = False
+    n_upd = steps * (1 + len(coefs))
+    k = 0
+
+    def update(first, th, cd, cz, zero):
+        nonlocal filled, k
+        k += 1
+        fill = fuse and (k < n_upd or fill_last)
+        args = (n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None if zero else dv.ptr(ax), dv.ptr(inv_d), first, th, cd, cz,
+                int(zero), None)
+        if fill:
+            check(L.hf_cheb_step_fill(*args, mask, dv.ptr(ax), dv.stream()))
+        else:
+            check(L.hf_cheb_step(*args, dv.stream()))
+        filled = fill
+
     for step in range(steps):
         zero = x_zero and step == 0
         if not zero:
-            _apply_into(apply_fn, x, ax)
-        check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None if zero else dv.ptr(ax), dv.ptr(inv_d), 1,
-                             theta, 0.0, 0.0, int(zero), None, dv.stream()))
+            _apply_maybe_filled(apply_fn, x, ax, filled)
+        update(1, theta, 0.0, 0.0, zero)
         for cd, cz in coefs:
-            _apply_into(apply_fn, x, ax)
-            check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), dv.ptr(ax), dv.ptr(inv_d), 0, 0.0, cd, cz, 0,
-                                 None, dv.stream()))
-    return x
+            _apply_maybe_filled(apply_fn, x, ax, filled)
+            update(0, 0.0, cd, cz, False)
+    return filled
 
 
 def chebyshev_apply(apply_fn, inv_diagonal, lam_max: float, b, x, settings: ChebyshevSettings = ChebyshevSettings(),
@@ -261,8 +289,10 @@ class LevelOperator:
     def smooth(self, b, x, steps: int, settings: ChebyshevSettings):
         return chebyshev_apply(self.op, self.inv_diag, self.lam_max, b, x, settings, steps)
 
-    def smooth_into(self, b, x, steps, settings, x_zero=False):
-        return _chebyshev_into(self.op, self.inv_diag, self.lam_max, b, x, self.d, self.ax, settings, steps, x_zero)
+    def smooth_into(self, b, x, steps, settings, x_zero=False, fill_last=False):
+        """Returns whether self.ax now holds mask ? x : 0 for the next apply."""
+        return _chebyshev_into(self.op, self.inv_diag, self.lam_max, b, x, self.d, self.ax, settings, steps, x_zero,
+                               mask=self.problem.mask_ptr(), fill_last=fill_last)
 
     def coarse_settings(self, settings: ChebyshevSettings) -> ChebyshevSettings:
         """Range widened to the estimated smallest eigenvalue (multigrid.py:248-252)."""
@@ -293,17 +323,22 @@ def _coarse_solve_into(level: LevelOperator, b, x, rel_target=1e-3, max_applicat
     # scal[0] = ||b||^2, scal[1] = rel_target * ||b||, flag = (||b|| == 0)
     dv.dot(b, b, scal[0:1])
     check(L.hf_scalar_op(1, dv.ptr(scal), 0, 1, rel_target, dv.ptr(flag), dv.stream()))
-    # x = 0 + inv_d b / theta
-    check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None, dv.ptr(level.inv_diag), 1, theta, 0.0, 0.0, 1,
-                         None, dv.stream()))
+    # x = 0 + inv_d b / theta; ax = mask ? x : 0 for the first application
+    mask = level.problem.mask_ptr()
+    check(L.hf_cheb_step_fill(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None, dv.ptr(level.inv_diag), 1, theta, 0.0, 0.0, 1,
+                              None, mask, dv.ptr(ax), dv.stream()))
     rho_old = 1.0 / sigma
     for step in range(2, max_applications + 1):
-        level.op.apply_into(x, ax, flag)
+        level.op.apply_after_fill(x, ax, flag)
         if step % s.degree == 0:
             check(L.hf_resnorm_check(ws, n, dv.ptr(b), dv.ptr(ax), dv.ptr(scal), 2, 1, dv.ptr(flag), dv.stream()))
         rho = 1.0 / (2.0 * sigma - rho_old)
-        check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), dv.ptr(ax), dv.ptr(level.inv_diag), 0, 0.0,
-                             rho * rho_old, 2.0 * rho / delta, 0, dv.ptr(flag), dv.stream()))
+        args = (n, dv.ptr(x), dv.ptr(d), dv.ptr(b), dv.ptr(ax), dv.ptr(level.inv_diag), 0, 0.0, rho * rho_old,
+                2.0 * rho / delta, 0, dv.ptr(flag))
+        if step < max_applications:  # the update also prepares the next application
+            check(L.hf_cheb_step_fill(*args, mask, dv.ptr(ax), dv.stream()))
+        else:
+            check(L.hf_cheb_step(*args, dv.stream()))
         rho_old = rho
     return x
 
@@ -326,8 +361,8 @@ def _v_cycle_into(levels, transfers, b, x, lvl, steps, settings):
         return _coarse_solve_into(levels[0], b, x, settings=settings)
     L = levels[lvl]
     C = levels[lvl - 1]
-    L.smooth_into(b, x, steps, settings, x_zero=True)
-    L.op.apply_into(x, L.ax)
+    filled = L.smooth_into(b, x, steps, settings, x_zero=True, fill_last=True)
+    _apply_maybe_filled(L.op, x, L.ax, filled)
     check(lib().hf_resid_masked(b.numel(), dv.ptr(L.r), dv.ptr(b), dv.ptr(L.ax), L.problem.mask_ptr(), dv.stream()))
     transfers[lvl - 1].restrict_into(L.r, C.b, mode=1)
     _v_cycle_into(levels, transfers, C.b, C.x, lvl - 1, steps, settings)

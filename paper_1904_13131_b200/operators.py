@@ -297,6 +297,12 @@ class MatrixFreeTangent:
         check(lib().hf_tangent_apply_flagged(self._op, dv.ptr(x), dv.ptr(y), dv.ptr(skip), dv.stream()))
         return y
 
+    def apply_after_fill(self, x: torch.Tensor, y: torch.Tensor, skip: torch.Tensor | None = None) -> torch.Tensor:
+        """Cell kernel of y = A x when the previous kernel on the stream already
+        wrote x and y = mask ? x : 0 (hf_cheb_step_fill); programmatic dependent launch."""
+        check(lib().hf_tangent_apply_after_fill(self._op, dv.ptr(x), dv.ptr(y), dv.ptr(skip), dv.stream()))
+        return y
+
     def apply_raw(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
         """y += sum over cells of A_loc x (constrained rows dropped), no init."""
         check(lib().hf_tangent_apply_raw(self._op, dv.ptr(x), dv.ptr(y), None, dv.stream()))
