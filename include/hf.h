@@ -104,6 +104,15 @@ HF_API int hf_tangent_apply_raw(hf_tangent* op, const double* x_dev, double* y_d
  * wrote x and y = mask ? x : 0 (hf_cheb_step_fill); programmatic dependent launch */
 HF_API int hf_tangent_apply_after_fill(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
                                        void* stream);
+/* Cell-range form of the accumulate-only apply, for overlapping a multi-GPU
+ * interface exchange with interior cells.  Cells are processed
+ * in tiles of `cells_per_tile` consecutive cells; tiles [tile0, tile1) are
+ * accumulated into y.  mode: 0 plain (y initialised earlier), 1 programmatic
+ * dependent of the y = mask ? x : 0 fill, 2 programmatic dependent of a
+ * kernel that wrote x and y. */
+HF_API int hf_tangent_tiles(const hf_tangent* op, long long* n_tiles, int* cells_per_tile);
+HF_API int hf_tangent_apply_tiles(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                  long long tile0, long long tile1, int mode, void* stream);
 /* .diagonal (395-410) */
 HF_API int hf_tangent_diagonal(hf_tangent* op, double* diag_dev, void* stream);
 /* .storage_bytes (412-417), cache.payload_scalars_per_qpoint / payload_nbytes (244-289) */

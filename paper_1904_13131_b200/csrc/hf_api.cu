@@ -271,6 +271,7 @@ HF_API int hf_space_destroy(hf_space* sp) {
 static CellArgs base_args(const hf_space* sp) {
   CellArgs a;
   std::memset(&a, 0, sizeof(a));
+  a.tile1 = -1;
   a.tab = sp->tab;
   a.lat = sp->lat;
   a.degree = sp->degree;
@@ -379,9 +380,11 @@ HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev,
 }
 
 static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev, int fill,
-                         void* stream) {
+                         void* stream, long long tile0 = 0, long long tile1 = -1) {
   if (!op || !x_dev || !y_dev) return fail(HF_ERR_ARG, "null argument");
   CellArgs a = base_args(op->sp);
+  a.tile0 = tile0;
+  a.tile1 = tile1;
   a.x = x_dev;
   a.y = y_dev;
   a.cache = op->d_cache;
@@ -420,6 +423,23 @@ HF_API int hf_tangent_apply_after_fill(hf_tangent* op, const double* x_dev, doub
                                        void* stream) {
   if (op && op->sp->lat.n_el == 0) return HF_OK;
   return tangent_apply(op, x_dev, y_dev, skip_dev, 2, stream);
+}
+
+HF_API int hf_tangent_tiles(const hf_tangent* op, long long* n_tiles, int* cells_per_tile) {
+  if (!op) return fail(HF_ERR_ARG, "null tangent");
+  const hf_space* sp = op->sp;
+  const int lines = sp->dim == 3 ? sp->n1 * sp->n1 : sp->n1;
+  const int cpw = 32 / lines;
+  if (cells_per_tile) *cells_per_tile = cpw;
+  if (n_tiles) *n_tiles = (sp->lat.n_el + cpw - 1) / cpw;
+  return HF_OK;
+}
+
+HF_API int hf_tangent_apply_tiles(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                  long long tile0, long long tile1, int mode, void* stream) {
+  if (mode < 0 || mode > 2 || tile0 < 0 || tile1 < tile0) return fail(HF_ERR_ARG, "bad tile range or mode");
+  if (!op || op->sp->lat.n_el == 0 || tile1 == tile0) return op ? HF_OK : fail(HF_ERR_ARG, "null tangent");
+  return tangent_apply(op, x_dev, y_dev, skip_dev, mode, stream, tile0, tile1);
 }
 
 HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream) {

@@ -65,7 +65,8 @@ struct CellArgs {
   const uint8_t* mask;      // [n_dofs] constrained DoFs
   const uint32_t* lmask;    // [n_el * lines] constraint bits per last-axis line (k_line_masks)
   const int* skip;          // optional device flag; non-zero -> kernel is a no-op
-  int fill;                 // apply: PDL secondary of the y = mask ? x : 0 fill kernel
+  int fill;                 // apply: 0 plain, 1/2 PDL secondary (hf_line.cuh LineArgs::fill)
+  long long tile0, tile1;   // apply: tile range; tile1 < 0 means all tiles
   unsigned long long* detmin;  // ordered-double min of det F (build / residual / range)
   unsigned long long* detmax;
 };

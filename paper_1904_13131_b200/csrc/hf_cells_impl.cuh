@@ -37,13 +37,16 @@ cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
   a.lmask = c.lmask;
   a.skip = c.skip;
   a.fill = c.fill;
+  const long long all_tiles = (c.lat.n_el + K::CPW - 1) / K::CPW;
+  a.tile0 = c.tile1 < 0 ? 0 : c.tile0;
+  a.tile1 = c.tile1 < 0 ? all_tiles : (c.tile1 < all_tiles ? c.tile1 : all_tiles);
   TabLine<N> T;
   for (int l = 0; l < N; ++l)
     for (int o = 0; o < N; ++o) {
       T.V[l][o] = c.tab.V[l * N + o];
       T.Dc[l][o] = c.tab.Dc[l * N + o];
     }
-  const long long tiles = (c.lat.n_el + K::CPW - 1) / K::CPW;
+  const long long tiles = a.tile1 - a.tile0;
   long long nb = (tiles + PL::W - 1) / PL::W;
   if (nb > resident) nb = resident;
   if (nb <= 0) return cudaSuccess;

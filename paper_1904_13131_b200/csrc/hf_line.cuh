@@ -68,6 +68,7 @@ struct LineArgs {
   // 1: PDL secondary of the y = mask ? x : 0 fill (operators.py:333-338): wait before the first scatter
   // 2: PDL secondary of a kernel that wrote x and y (hf_cheb_step_fill): wait before the first gather
   int fill;
+  long long tile0, tile1;  // tile range of this launch (interior/boundary split of a slab)
 };
 
 // Per-warp line-buffer layout: element (cell m, component c, point i,j,k) at
@@ -327,11 +328,11 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
   double* ring = smem + (size_t)warp * RW * CH;  // this warp's stages (16-byte aligned)
   double* lbuf = smem + (size_t)W * RW * CH;      // W x NB x BUF
   unsigned long long* full = reinterpret_cast<unsigned long long*>(lbuf + (size_t)W * NB * Y::BUF) + warp * RW;
-  const long long ntiles = (a.lat.n_el + K::CPW - 1) / K::CPW;
+  const long long ntiles = a.tile1;  // tiles [a.tile0, a.tile1) of the (CPW-cell) tiling
   const long long tstride = (long long)N * CH;
-  // chunk j of this warp: tile blockIdx.x + (warp + (j / N) * W) * gridDim.x, iq = j % N
+  // chunk j of this warp: tile tile0 + blockIdx.x + (warp + (j / N) * W) * gridDim.x, iq = j % N
   auto issue = [&](long long j) {
-    const long long tile = blockIdx.x + (warp + (j / N) * W) * (long long)gridDim.x;
+    const long long tile = a.tile0 + blockIdx.x + (warp + (j / N) * W) * (long long)gridDim.x;
     if (tile >= ntiles) return;
     const int s = (int)(j % RW);
     mbar_expect_tx(full + s, (unsigned)(CH * sizeof(double)));
@@ -366,8 +367,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
   long long jc = 0;  // this warp's chunk counter
   const long long tstep = (long long)W * gridDim.x;
   Gather<DIM, N, VAR> nxt;
-  gather_tile<DIM, N, VAR>(a, blockIdx.x + (long long)warp * gridDim.x, ntiles, m, t, act, nxt);
-  for (long long tile = blockIdx.x + (long long)warp * gridDim.x; tile < ntiles; tile += tstep) {
+  gather_tile<DIM, N, VAR>(a, a.tile0 + blockIdx.x + (long long)warp * gridDim.x, ntiles, m, t, act, nxt);
+  for (long long tile = a.tile0 + blockIdx.x + (long long)warp * gridDim.x; tile < ntiles; tile += tstep) {
     const Gather<DIM, N, VAR> g = nxt;
     gather_tile<DIM, N, VAR>(a, tile + tstep, ntiles, m, t, act, nxt);  // in flight during this tile
     const long long e = g.e;

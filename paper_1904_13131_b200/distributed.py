@@ -63,8 +63,26 @@ class LocalComm:
         if sends or recvs:
             raise ValueError("a single rank has no neighbours")
 
+    def exchange_start(self, sends: dict, recvs: dict):
+        self.exchange(sends, recvs)
+        return _Done()
+
     def barrier(self) -> None:
         pass
+
+
+class _Done:
+    def wait(self):
+        pass
+
+
+class _Works:
+    def __init__(self, works):
+        self.works = works
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
 
 
 class TorchComm:
@@ -87,6 +105,17 @@ class TorchComm:
         else:
             self.dist.all_reduce(t, group=self.group)
         return t
+
+    def exchange_start(self, sends: dict, recvs: dict):
+        """Start the swap; returns a handle whose ``wait()`` orders the current
+        stream after it (NCCL: asynchronous on the device; staged: completed here)."""
+        if self.staged:
+            self.exchange(sends, recvs)
+            return _Done()
+        dist = self.dist
+        ops = [dist.P2POp(dist.isend, sends[p], p, self.group) for p in sorted(sends)]
+        ops += [dist.P2POp(dist.irecv, recvs[p], p, self.group) for p in sorted(recvs)]
+        return _Works(dist.batch_isend_irecv(ops) if ops else [])
 
     def exchange(self, sends: dict, recvs: dict) -> None:
         """Point-to-point swap: ``sends[peer]`` -> peer, ``recvs[peer]`` <- peer."""
@@ -288,6 +317,18 @@ class SlabExchange:
         self.recv = {p: torch.empty(pd, dtype=torch.float64, device=mask_dev.device) for p in self.peers}
         self.mask = {p: mask_dev[s] for p, s in self.peers.items()}
 
+    def start(self, y: torch.Tensor):
+        """Post the interface planes of y (their partial sums must be final);
+        ``finish`` adds the neighbours' partials.  The interior cells may run in between."""
+        sends = {p: y[s] for p, s in self.peers.items()}  # contiguous views: no copy
+        return self.comm.exchange_start(sends, self.recv)
+
+    def finish(self, handle, y: torch.Tensor) -> torch.Tensor:
+        handle.wait()
+        for p, s in self.peers.items():
+            self.add_fn(y[s], self.recv[p], self.mask[p])
+        return y
+
     def add(self, y: torch.Tensor) -> torch.Tensor:
         if not self.peers:
             return y
@@ -361,13 +402,49 @@ class DistributedTangent:
         _agree_jacobian(dp.comm, err, level)
         self.strategy = strategy
 
+        self._split = self._tile_split()
+
+    def _tile_split(self):
+        """(boundary tile ranges, interior tile range) of the slab: the boundary
+        tiles hold every cell of the first / last cell layer that touches an
+        interface plane, so the planes' partial sums are final after them."""
+        sl = self.dp.slab
+        if not (sl.has_lower or sl.has_upper):
+            return None
+        nt, cpt = self.local.tiles()
+        cells = self.dp.local.mesh.cells
+        layer = int(np.prod(cells[:-1]))
+        n_el = self.dp.local.mesh.n_elements
+        lo = -(-layer // cpt) if sl.has_lower else 0
+        hi = (n_el - layer) // cpt if sl.has_upper else nt
+        if lo >= hi:
+            return None
+        bounds = [(0, lo)] if lo > 0 else []
+        if hi < nt:
+            bounds.append((hi, nt))
+        return bounds, (lo, hi)
+
     @property
     def n_dofs(self) -> int:
         return self.dp.n_dofs
 
     def apply_into(self, x: torch.Tensor, y: torch.Tensor, skip=None) -> torch.Tensor:
-        self.local.apply_into(x, y, skip)
-        return self.dp.exchange.add(y)
+        """y = A x on the slab.  The interface exchange overlaps the interior cells:
+        fill, boundary tiles, post the planes, interior tiles, add the partials."""
+        if skip is not None or self._split is None:
+            self.local.apply_into(x, y, skip)
+            return self.dp.exchange.add(y)
+        bounds, (i0, i1) = self._split
+        check(lib().hf_fill_masked(x.numel(), dv.ptr(y), dv.ptr(x), dv.ptr(self.dp.mask_dev), 0.0, dv.stream()))
+        for k, (t0, t1) in enumerate(bounds):
+            self.local.apply_tiles(x, y, t0, t1, mode=1 if k == 0 else 0)
+        ex = self.dp.exchange
+        with ex.timer.span("exchange"):
+            h = ex.start(y)
+        self.local.apply_tiles(x, y, i0, i1, mode=0)
+        with ex.timer.span("exchange"):
+            ex.finish(h, y)
+        return y
 
     def apply(self, x: torch.Tensor) -> torch.Tensor:
         y = torch.empty_like(x)

@@ -303,6 +303,18 @@ class MatrixFreeTangent:
         check(lib().hf_tangent_apply_after_fill(self._op, dv.ptr(x), dv.ptr(y), dv.ptr(skip), dv.stream()))
         return y
 
+    def tiles(self) -> tuple[int, int]:
+        """(number of tiles, cells per tile) of the cell kernel's work decomposition."""
+        nt, cpt = ct.c_longlong(), ct.c_int()
+        check(lib().hf_tangent_tiles(self._op, ct.byref(nt), ct.byref(cpt)))
+        return nt.value, cpt.value
+
+    def apply_tiles(self, x: torch.Tensor, y: torch.Tensor, tile0: int, tile1: int, mode: int = 0) -> torch.Tensor:
+        """y += A_loc x over the cells of tiles [tile0, tile1) (constrained rows dropped);
+        mode 1/2: programmatic dependent of the fill / of an x-and-y producer."""
+        check(lib().hf_tangent_apply_tiles(self._op, dv.ptr(x), dv.ptr(y), None, tile0, tile1, mode, dv.stream()))
+        return y
+
     def apply_raw(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
         """y += sum over cells of A_loc x (constrained rows dropped), no init."""
         check(lib().hf_tangent_apply_raw(self._op, dv.ptr(x), dv.ptr(y), None, dv.stream()))
