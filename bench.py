@@ -392,9 +392,44 @@ def _extras(args, hbm, prob, ubar, x, y, flush, nqp):
     y3 = torch.empty_like(x3)
     nq3 = p3.mesh.n_elements * p3.n_qpoints_per_cell
     out["cfg3_q4"] = {s: variant(p3, wl3.ubar, x3, y3, s, nq3) for s in ("tensor4", "tensor2", "scalar")}
+    out["matrix_based"] = _matrix_based(prob, ubar, x, flush, hbm)
     if not args.no_newton:
         out["newton"] = _newton_iteration()
     return out
+
+
+def _matrix_based(prob, ubar, x, flush, hbm):
+    """The paper's comparison on B200: the assembled CSR tangent (GPU element
+    matrices, cuSPARSE SpMV; operators.py:436-516) against the matrix-free apply."""
+    import torch
+
+    from paper_1904_13131_b200 import AssembledTangent
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    op = AssembledTangent(prob, ubar)
+    torch.cuda.synchronize()
+    t_asm = time.perf_counter() - t0
+    y = torch.empty_like(x)
+    for _ in range(3):
+        op.apply_into(x, y)
+    ts = []
+    for _ in range(10):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        op.apply_into(x, y)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    nnz = op.matrix.values().numel()
+    csr_bytes = 8 * nnz + 8 * nnz + 8 * (prob.n_dofs + 1)  # torch keeps 64-bit indices
+    return {"assembly_s": t_asm, "spmv_ms": ms, "GDoF_s": prob.n_dofs / ms / 1e6, "nnz": nnz,
+            "storage_bytes_reference_convention": op.storage_bytes(),
+            "spmv_GBs": (csr_bytes + 16 * prob.n_dofs) / ms / 1e6,
+            "spmv_frac_hbm": (csr_bytes + 16 * prob.n_dofs) / ms / 1e6 / hbm,
+            "note": "cuSPARSE SpMV via torch (library baseline); matrix-free tensor4 apply is the comparison"}
 
 
 def _cfg5(comm, steps: int, warmup: int):

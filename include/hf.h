@@ -113,6 +113,12 @@ HF_API int hf_tangent_apply_after_fill(hf_tangent* op, const double* x_dev, doub
 HF_API int hf_tangent_tiles(const hf_tangent* op, long long* n_tiles, int* cells_per_tile);
 HF_API int hf_tangent_apply_tiles(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
                                   long long tile0, long long tile1, int mode, void* stream);
+/* matrix-based baseline (assemble_matrix / AssembledTangent, operators.py:436-516):
+ * vals_dev (n_el, nld, nld) element matrices of a tensor4 tangent, nld = nloc*dim,
+ * local DoF n*dim + c; dofs_dev (n_el, nld) their global DoFs (operators.py:474).
+ * 3D Q1-Q2 and 2D Q1-Q4. */
+HF_API int hf_tangent_assemble_local(hf_tangent* op, double* vals_dev, void* stream);
+HF_API int hf_space_cell_dofs(const hf_space* sp, long long* dofs_dev, void* stream);
 /* .diagonal (395-410) */
 HF_API int hf_tangent_diagonal(hf_tangent* op, double* diag_dev, void* stream);
 /* .storage_bytes (412-417), cache.payload_scalars_per_qpoint / payload_nbytes (244-289) */

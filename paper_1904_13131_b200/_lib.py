@@ -51,6 +51,8 @@ _SIGS = {
     "hf_tangent_tiles": (I, [P, ct.POINTER(LL), ct.POINTER(I)]),
     "hf_tangent_apply_tiles": (I, [P, P, P, P, LL, LL, I, P]),
     "hf_tangent_diagonal": (I, [P, P, P]),
+    "hf_tangent_assemble_local": (I, [P, P, P]),
+    "hf_space_cell_dofs": (I, [P, P, P]),
     "hf_tangent_storage": (I, [P, ct.POINTER(LL), ct.POINTER(I), ct.POINTER(LL)]),
     "hf_tangent_destroy": (I, [P]),
     "hf_residual": (I, [P, P, P, P, P, P, ct.POINTER(HfErrorInfo)]),

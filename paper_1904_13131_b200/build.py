@@ -19,7 +19,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build_obj")
 LIB = os.path.join(PKG, "libhf.so")
-SOURCES = ["hf_api.cu", "hf_cells2d.cu", "hf_cells3d.cu"]
+SOURCES = ["hf_api.cu", "hf_cells2d.cu", "hf_cells3d.cu", "hf_assemble.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-I", os.path.join(ROOT, "include")]

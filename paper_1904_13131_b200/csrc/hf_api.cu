@@ -446,6 +446,24 @@ HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, 
   return hf_tangent_apply_flagged(op, x_dev, y_dev, nullptr, stream);
 }
 
+HF_API int hf_tangent_assemble_local(hf_tangent* op, double* vals_dev, void* stream) {
+  if (!op || !vals_dev) return fail(HF_ERR_ARG, "null argument");
+  if (op->strategy != HF_TENSOR4) return fail(HF_ERR_ARG, "element matrices are formed from a tensor4 cache");
+  const hf_space* sp = op->sp;
+  if ((sp->dim == 3 && sp->n1 > 3) || (sp->dim == 2 && sp->n1 > 5))
+    return fail(HF_ERR_UNSUPPORTED, "matrix-based assembly is instantiated for 3D Q1-Q2 and 2D Q1-Q4");
+  CellArgs a = base_args(sp);
+  a.cache = op->d_cache;
+  HF_CUDA(launch_assemble(sp->dim, sp->n1, a, vals_dev, S(stream)));
+  return HF_OK;
+}
+
+HF_API int hf_space_cell_dofs(const hf_space* sp, long long* dofs_dev, void* stream) {
+  if (!sp || !dofs_dev) return fail(HF_ERR_ARG, "null argument");
+  HF_CUDA(launch_cell_dofs(sp->lat, sp->dim, sp->degree, dofs_dev, S(stream)));
+  return HF_OK;
+}
+
 HF_API int hf_tangent_diagonal(hf_tangent* op, double* d_dev, void* stream) {
   if (!op || !d_dev) return fail(HF_ERR_ARG, "null argument");
   const hf_space* sp = op->sp;

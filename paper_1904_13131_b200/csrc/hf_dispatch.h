@@ -15,6 +15,10 @@ cudaError_t launch_cell_3d(int op, int n1, int var, const CellArgs& a, int mode,
 cudaError_t launch_geometry(int dim, const HfTables& tab, const HfLattice& lat, int nq1, const double* verts,
                             double* jinv, double* jxw, unsigned long long* detmin, cudaStream_t s);
 
+// element matrices of the matrix-based baseline (hf_assemble.cu)
+cudaError_t launch_assemble(int dim, int n1, const CellArgs& a, double* vals, cudaStream_t s);
+cudaError_t launch_cell_dofs(const HfLattice& lat, int dim, int degree, long long* dofs, cudaStream_t s);
+
 // blocks per grid and cells per block of the cell kernels
 int cells_per_block(int dim, int n1);
 

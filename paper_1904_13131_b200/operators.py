@@ -14,6 +14,7 @@ reference's calling convention) or CUDA fp64 torch tensors (stay on device).
 from __future__ import annotations
 
 import ctypes as ct
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -348,8 +349,78 @@ class MatrixFreeTangent:
         return self._storage
 
 
+class AssembledTangent:
+    """Matrix-based tangent: CSR on the device, used as baseline and second
+    oracle (operators.py:436-516).
+
+    Element matrices come from libhf (``hf_tangent_assemble_local``, formed
+    from the tensor4 q-point cache); duplicates are summed and the CSR built
+    with torch's sort/coalesce; constrained rows and columns are cleared and
+    replaced by a unit diagonal (operators.py:481-490); ``apply`` is a
+    cuSPARSE SpMV.  Host-side plumbing only: a baseline, not the hot path."""
+
+    strategy = "matrix_based"
+
+    def __init__(self, problem: Problem, u_bar):
+        self.problem = problem
+        op4 = MatrixFreeTangent(problem, u_bar, "tensor4")  # NonPositiveJacobian propagates
+        nel, d = problem.mesh.n_elements, problem.dim
+        nld = problem.n_qpoints_per_cell * d
+        vals = torch.empty(nel * nld * nld, dtype=torch.float64, device="cuda")
+        check(lib().hf_tangent_assemble_local(op4._op, dv.ptr(vals), dv.stream()))
+        dofs = torch.empty(nel * nld, dtype=torch.int64, device="cuda")
+        check(lib().hf_space_cell_dofs(problem._space, dv.ptr(dofs), dv.stream()))
+        del op4
+        dofs = dofs.view(nel, nld)
+        rows = dofs[:, :, None].expand(nel, nld, nld).reshape(-1)
+        cols = dofs[:, None, :].expand(nel, nld, nld).reshape(-1)
+        mask = problem.mask_dev
+        keep = ~(mask[rows] | mask[cols])
+        fixed = torch.nonzero(mask).reshape(-1)
+        rows = torch.cat([rows[keep], fixed])
+        cols = torch.cat([cols[keep], fixed])
+        vals = torch.cat([vals[keep], torch.ones(fixed.numel(), dtype=torch.float64, device="cuda")])
+        n = problem.n_dofs
+        coo = torch.sparse_coo_tensor(torch.stack([rows, cols]), vals, (n, n), check_invariants=False).coalesce()
+        del rows, cols, vals, keep
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)  # "sparse CSR support is in beta"
+            self.matrix = coo.to_sparse_csr()
+        self._diag = None
+
+    @property
+    def n_dofs(self) -> int:
+        return self.problem.n_dofs
+
+    def apply_into(self, x: torch.Tensor, y: torch.Tensor, skip=None) -> torch.Tensor:
+        y.copy_(torch.mv(self.matrix, x))
+        return y
+
+    def apply(self, x):
+        xd = dv.as_dev(x)
+        return dv.like_input(torch.mv(self.matrix, xd), x)
+
+    __call__ = apply
+
+    def diagonal(self):
+        if self._diag is None:
+            m = self.matrix
+            crow, col, val = m.crow_indices(), m.col_indices(), m.values()
+            row = torch.repeat_interleave(torch.arange(self.n_dofs, device="cuda"), crow[1:] - crow[:-1])
+            d = torch.zeros(self.n_dofs, dtype=torch.float64, device="cuda")
+            on = row == col
+            d.index_add_(0, row[on], val[on])
+            self._diag = d
+        return self._diag
+
+    def storage_bytes(self) -> int:
+        """CSR bytes with 32-bit indices, as scipy stores the reference matrix (operators.py:514-516)."""
+        nnz = self.matrix.values().numel()
+        return 8 * nnz + 4 * nnz + 4 * (self.n_dofs + 1)
+
+
 def make_tangent(problem: Problem, u_bar, strategy: str):
-    """(operators.py:519-522).  The CSR "matrix_based" baseline is a SURVEY §8(f) next row."""
+    """(operators.py:519-522)"""
     if strategy == "matrix_based":
-        raise NotImplementedError("matrix_based (CSR) tangent is not part of the B200 hot path yet")
+        return AssembledTangent(problem, u_bar)
     return MatrixFreeTangent(problem, u_bar, strategy)
