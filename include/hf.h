@@ -132,6 +132,11 @@ HF_API int hf_tangent_destroy(hf_tangent* op);
 HF_API int hf_residual(hf_space* sp, const double* u_dev, const double* traction, const double* surf_w_dev,
                        double* out_dev, void* stream, hf_error_info* err);
 
+/* ---- energy (operators.py:227-236): out_dev[0] = sum_q psi(F) JxW, the
+ * strain energy without the traction work (the host subtracts
+ * traction . (surface_weights u)); HF_ERR_JACOBIAN as hf_residual */
+HF_API int hf_energy(hf_space* sp, const double* u_dev, double* out_dev, void* stream, hf_error_info* err);
+
 /* ---- TransferOperator (multigrid.py:27-73) ----
  * interp_1d[a]: host (n_fine_a, n_coarse_a) row-major 1D interpolation matrix
  * of axis a (_interpolation_matrix_1d, multigrid.py:58-73).

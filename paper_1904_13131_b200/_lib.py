@@ -56,6 +56,7 @@ _SIGS = {
     "hf_tangent_storage": (I, [P, ct.POINTER(LL), ct.POINTER(I), ct.POINTER(LL)]),
     "hf_tangent_destroy": (I, [P]),
     "hf_residual": (I, [P, P, P, P, P, P, ct.POINTER(HfErrorInfo)]),
+    "hf_energy": (I, [P, P, P, P, ct.POINTER(HfErrorInfo)]),
     "hf_transfer_create": (I, [P, P, ct.POINTER(P), ct.POINTER(P)]),
     "hf_prolong": (I, [P, P, P, I, P]),
     "hf_restrict": (I, [P, P, P, I, P]),

@@ -528,6 +528,25 @@ HF_API int hf_residual(hf_space* sp, const double* u_dev, const double* traction
   return HF_OK;
 }
 
+HF_API int hf_energy(hf_space* sp, const double* u_dev, double* out_dev, void* stream, hf_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!sp || !u_dev || !out_dev) return fail(HF_ERR_ARG, "null argument");
+  cudaStream_t s = S(stream);
+  HF_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), s));
+  unsigned long long init = ~0ull;
+  HF_CUDA(cudaMemcpyAsync(sp->d_u64, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+  CellArgs a = base_args(sp);
+  a.x = u_dev;
+  a.y = out_dev;
+  a.detmin = sp->d_u64;
+  HF_CUDA(cell(sp, OP_ENERGY, 0, a, s));
+  unsigned long long o;
+  HF_CUDA(cudaMemcpyAsync(&o, sp->d_u64, sizeof(o), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  if (sp->lat.n_el > 0 && !(hf_unord(o) > 0.0)) return locate_min_det(sp, u_dev, s, err);
+  return HF_OK;
+}
+
 // ---------------------------------------------------------------------------
 HF_API int hf_transfer_create(const hf_space* coarse, const hf_space* fine, const double* const* interp_1d,
                               hf_transfer** out) {

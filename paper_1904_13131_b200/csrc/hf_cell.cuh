@@ -718,6 +718,53 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_jrange(const CellArgs a, in
 }
 
 // ---------------------------------------------------------------------------
+// total strain energy sum_q psi(F) JxW (operators.py:227-236, material.py:98-106):
+// psi = mu/2 (tr C - d - 2 ln J) + lam (ln J)^2, block partials atomically
+// added into *a.y; min det F into a.detmin (NonPositiveJacobian)
+// ---------------------------------------------------------------------------
+template <int DIM, int N>
+__global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_energy(const CellArgs a) {
+  using K = Cfg<DIM, N>;
+  constexpr int NQ = K::NQ;
+  extern __shared__ double sm[];
+  load_tables<DIM, N>(sm, a.tab, false);
+  Team t = make_team<DIM, N>(a.lat, a.degree);
+  double* A = sm + K::TAB + t.slot * K::SBUF;
+  double* B = A + K::CPB * K::SBUF;
+  const long long qi = t.e * NQ + t.lq;
+  gather_nodal<DIM, N>(a.x, nullptr, t, A);
+  __syncthreads();
+  double gu[DIM][DIM];
+  eval_gradients<DIM, N>(A, B, sm, t, gu);
+  double J = 1.0, psi = 0.0;
+  if (t.act) {
+    double ji[DIM][DIM];
+    load_jinv<DIM>(a, qi, ji);
+    double F[DIM * DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i)
+#pragma unroll
+      for (int Aa = 0; Aa < DIM; ++Aa) {
+        double s = (i == Aa) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < DIM; ++q) s = fma(gu[i][q], ji[q][Aa], s);
+        F[i * DIM + Aa] = s;
+      }
+    J = hf_det<DIM>(F);
+    double trc = 0.0;
+#pragma unroll
+    for (int k = 0; k < DIM * DIM; ++k) trc = fma(F[k], F[k], trc);  // tr C = |F|^2
+    const double lnj = log(J);
+    const double mu = __ldg(a.mu + t.e), lam = __ldg(a.lam + t.e);
+    psi = (0.5 * mu * (trc - DIM - 2.0 * lnj) + lam * lnj * lnj) * __ldg(a.jxw + qi);
+  }
+  warp_minmax_atomic(a.detmin, nullptr, J, t.act);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) psi += __shfl_xor_sync(0xffffffffu, psi, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(a.y, psi);
+}
+
+// ---------------------------------------------------------------------------
 // geometry cache (mesh.py:290-307): one thread per (cell, q-point)
 // ---------------------------------------------------------------------------
 template <int DIM>

@@ -94,6 +94,9 @@ cudaError_t launch_one(int op, int var, const CellArgs& a, int mode, double targ
     case OP_RESIDUAL:
       k_residual<DIM, N><<<grid, block, sm, s>>>(a);
       break;
+    case OP_ENERGY:
+      k_energy<DIM, N><<<grid, block, sm, s>>>(a);
+      break;
     case OP_JRANGE:
       k_jrange<DIM, N><<<grid, block, sm, s>>>(a, mode, target, first);
       break;

@@ -5,7 +5,7 @@
 
 namespace hf {
 
-enum CellOp { OP_APPLY = 0, OP_BUILD = 1, OP_DIAG = 2, OP_RESIDUAL = 3, OP_JRANGE = 4 };
+enum CellOp { OP_APPLY = 0, OP_BUILD = 1, OP_DIAG = 2, OP_RESIDUAL = 3, OP_JRANGE = 4, OP_ENERGY = 5 };
 
 // Returns cudaErrorInvalidValue when (dim, n1) is not instantiated.
 cudaError_t launch_cell_2d(int op, int n1, int var, const CellArgs& a, int mode, double target,

@@ -250,6 +250,24 @@ def compute_residual(problem: Problem, u, traction=None):
     return dv.like_input(out, u)
 
 
+def energy(problem: Problem, u, traction=None) -> float:
+    """Total potential energy: strain energy minus the top traction work
+    (operators.py:227-236); the finite-difference oracle of the residual."""
+    ud = dv.as_dev(u)
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    err = HfErrorInfo()
+    rc = lib().hf_energy(problem._space, dv.ptr(ud), dv.ptr(out), dv.stream(), ct.byref(err))
+    if rc == HF_ERR_JACOBIAN:
+        _raise_jacobian(err)
+    check(rc)
+    total = float(out.item())
+    if traction is not None:
+        t = torch.as_tensor(np.asarray(traction, dtype=np.float64).reshape(-1), device="cuda")
+        work = problem.surface_weights_dev @ ud.view(-1, problem.dim)  # (dim,)
+        total -= float(t @ work)
+    return total
+
+
 @dataclass
 class CacheInfo:
     """What the reference exposes of its quadrature caches (operators.py:244-289)."""

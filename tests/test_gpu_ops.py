@@ -131,3 +131,32 @@ def test_constraints_override_changes_device_mask(lib_loaded):
     op_.mask = np.zeros(p.n_dofs, dtype=bool)
     assert rel(y2, O.Tangent(op_, g["ubar"], "tensor4").apply(g["x"])) < TOL
     assert rel(y1, g["y_tensor4"]) < TOL
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_energy_vs_reference(name, lib_loaded):
+    """Total potential energy (operators.py:227-236) against the reference value."""
+    from paper_1904_13131_b200 import NonPositiveJacobian, energy
+
+    g = golden(name)
+    p = product_problem(g)
+    e = energy(p, g["ubar"], g["traction"])
+    assert abs(e - float(g["energy"])) <= 1e-12 * abs(float(g["energy"]))
+    with pytest.raises(NonPositiveJacobian):
+        energy(p, g["bad_state"])
+
+
+@pytest.mark.parametrize("name", ["ops_2d_q2.npz", "ops_3d_q2.npz"])
+def test_residual_is_energy_gradient(name, lib_loaded):
+    """verify.py:107-121: central differences of the energy along a direction
+    that vanishes on the constraints reproduce residual . v."""
+    from paper_1904_13131_b200 import compute_residual, energy
+
+    g = golden(name)
+    p = product_problem(g)
+    v = np.random.default_rng(4).standard_normal(p.n_dofs)
+    v[g["mask"]] = 0.0
+    eps = 1e-6
+    fd = (energy(p, g["ubar"] + eps * v, g["traction"]) - energy(p, g["ubar"] - eps * v, g["traction"])) / (2 * eps)
+    r = compute_residual(p, g["ubar"], g["traction"])
+    assert abs(fd - r @ v) <= 1e-6 * max(1.0, abs(r @ v))
