@@ -401,6 +401,7 @@ def _extras(args, hbm, prob, ubar, x, y, flush, nqp):
     out["matrix_based"] = _matrix_based(prob, ubar, x, flush, hbm)
     if not args.no_newton:
         out["newton"] = _newton_iteration()
+        out["newton_fp32_levels"] = _newton_iteration("fp32")
     return out
 
 
@@ -533,11 +534,12 @@ def _dist_newton(comm):
     return rec
 
 
-def _newton_iteration():
+def _newton_iteration(coarse_precision="fp64"):
     """First Newton iteration of load step 1 of config 4 (64^3 Q2, levels 4..64,
     prescribed top displacement): tangent + GMG build, CG to 1e-6
     (NewtonSettings.linear_rel_tol, solver.py:85), residual.  Run twice; the
-    second (warm) run is reported."""
+    second (warm) run is reported.  coarse_precision="fp32": every GMG level
+    below the finest in fp32 storage."""
     import torch
 
     from paper_1904_13131_b200 import MatrixFreeTangent, build_gmg, build_transfers, cg, compute_residual
@@ -557,7 +559,8 @@ def _newton_iteration():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         op = MatrixFreeTangent(fine, u, "tensor4")
-        gmg = build_gmg(probs, u, "tensor4", seed=0, transfers=transfers, keep_constrained=True)
+        gmg = build_gmg(probs, u, "tensor4", seed=0, transfers=transfers, keep_constrained=True,
+                        coarse_precision=coarse_precision)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         du, rep = cg(op, -res, rel_tol=1e-6, preconditioner=gmg)
@@ -568,6 +571,7 @@ def _newton_iteration():
         torch.cuda.synchronize()
         t3 = time.perf_counter()
         rec = {"workload": "cfg4 64^3 Q2 levels 4..64, load step 1, Newton iteration 1", "n_dofs": fine.n_dofs,
+               "coarse_levels": coarse_precision,
                "newton_iteration_s": t3 - t0, "setup_s": t1 - t0, "cg_s": t2 - t1, "cg_iterations": rep.iterations,
                "s_per_cg_iteration": (t2 - t1) / max(rep.iterations, 1)}
         del op, gmg

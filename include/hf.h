@@ -91,6 +91,12 @@ HF_API int hf_jacobian_range(hf_space* sp, const double* u_dev, void* stream, do
  * filled hf_error_info when det F <= 0 (the NonPositiveJacobian path). */
 HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev, void* stream, hf_tangent** out,
                              hf_error_info* err);
+/* mixed precision: storage_bits = 32 stores the q-point
+ * cache in float, and the tangent's x / y vectors are then float arrays too;
+ * all arithmetic stays fp64.  storage_bits = 64 is hf_tangent_create.  The
+ * diagonal and the element matrices need an fp64 tangent. */
+HF_API int hf_tangent_create_ex(hf_space* sp, int strategy, int storage_bits, const double* ubar_dev, void* stream,
+                                hf_tangent** out, hf_error_info* err);
 /* .apply (331-339): y = A x with zero-in / identity-out constrained handling */
 HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream);
 /* same, but a no-op while *skip_dev != 0 (device-side early exit for graphs) */
@@ -147,6 +153,12 @@ HF_API int hf_transfer_create(const hf_space* coarse, const hf_space* fine, cons
                               hf_transfer** out);
 HF_API int hf_prolong(hf_transfer* t, const double* xc_dev, double* xf_dev, int mode, void* stream);
 HF_API int hf_restrict(hf_transfer* t, const double* rf_dev, double* rc_dev, int mode, void* stream);
+/* the same with 32/64-bit input and output vectors (fp32 multigrid levels);
+ * passes run in fp64 */
+HF_API int hf_prolong_ex(hf_transfer* t, const void* xc_dev, int in_bits, void* xf_dev, int out_bits, int mode,
+                         void* stream);
+HF_API int hf_restrict_ex(hf_transfer* t, const void* rf_dev, int in_bits, void* rc_dev, int out_bits, int mode,
+                          void* stream);
 HF_API int hf_transfer_destroy(hf_transfer* t);
 /* restrict_solution, one level (multigrid.py:76-92); keep_constrained != 0
  * keeps prescribed (non-zero Dirichlet) values */
@@ -197,6 +209,18 @@ HF_API int hf_probe_dfma(long long iters, int blocks, int threads, double* sink_
  * analogue -- the paper's MPI ghost exchange):
  * y[i] += recv[i] where mask[i] == 0 */
 HF_API int hf_halo_add(long long n, double* y, const double* recv, const unsigned char* mask, void* stream);
+/* fp32-vector versions for mixed-precision levels (arithmetic in fp64;
+ * hf_cheb_step_f32 fills y_next = mask ? x : 0 when fill_mask != NULL) */
+HF_API int hf_fill_masked_f32(long long n, float* y, const float* x, const unsigned char* mask, double masked_value,
+                              void* stream);
+HF_API int hf_cheb_step_f32(long long n, float* x, float* d, const float* b, const float* ax, const float* inv_d,
+                            int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
+                            const unsigned char* fill_mask, float* y_next, void* stream);
+HF_API int hf_resid_masked_f32(long long n, float* r, const float* b, const float* ax, const unsigned char* mask,
+                               void* stream);
+HF_API int hf_dot_f32(hf_ws* w, long long n, const float* a, const float* b, double* out_dev, void* stream);
+HF_API int hf_resnorm_check_f32(hf_ws* w, long long n, const float* b, const float* ax, double* scal, int out_idx,
+                                int target_idx, int* flag_dev, void* stream);
 /* y = a x + b y */
 HF_API int hf_axpby(long long n, double a, const double* x, double b, double* y, void* stream);
 

@@ -44,6 +44,7 @@ _SIGS = {
     "hf_space_destroy": (I, [P]),
     "hf_jacobian_range": (I, [P, P, P, PD, PD, ct.POINTER(LL), ct.POINTER(I)]),
     "hf_tangent_create": (I, [P, I, P, P, ct.POINTER(P), ct.POINTER(HfErrorInfo)]),
+    "hf_tangent_create_ex": (I, [P, I, I, P, P, ct.POINTER(P), ct.POINTER(HfErrorInfo)]),
     "hf_tangent_apply": (I, [P, P, P, P]),
     "hf_tangent_apply_flagged": (I, [P, P, P, P, P]),
     "hf_tangent_apply_raw": (I, [P, P, P, P, P]),
@@ -60,6 +61,8 @@ _SIGS = {
     "hf_transfer_create": (I, [P, P, ct.POINTER(P), ct.POINTER(P)]),
     "hf_prolong": (I, [P, P, P, I, P]),
     "hf_restrict": (I, [P, P, P, I, P]),
+    "hf_prolong_ex": (I, [P, P, I, P, I, I, P]),
+    "hf_restrict_ex": (I, [P, P, I, P, I, I, P]),
     "hf_transfer_destroy": (I, [P]),
     "hf_inject": (I, [P, P, P, P, I, P]),
     "hf_ws_create": (I, [ct.POINTER(P)]),
@@ -75,6 +78,11 @@ _SIGS = {
     "hf_cg_update_p": (I, [LL, P, P, P, I, I, P]),
     "hf_jacobi_dot": (I, [P, LL, P, P, P, P, P]),
     "hf_axpby": (I, [LL, D, P, D, P, P]),
+    "hf_fill_masked_f32": (I, [LL, P, P, P, D, P]),
+    "hf_cheb_step_f32": (I, [LL, P, P, P, P, P, I, D, D, D, I, P, P, P, P]),
+    "hf_resid_masked_f32": (I, [LL, P, P, P, P, P]),
+    "hf_dot_f32": (I, [P, LL, P, P, P, P]),
+    "hf_resnorm_check_f32": (I, [P, LL, P, P, P, I, I, P, P]),
     "hf_halo_add": (I, [LL, P, P, P, P]),
     "hf_probe_dfma": (I, [LL, I, I, P, P]),
 }

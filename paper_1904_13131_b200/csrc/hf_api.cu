@@ -88,6 +88,7 @@ struct hf_tangent {
   hf_space* sp;
   int strategy;
   int nf;
+  int fp32 = 0;  // cache and x/y stored as float (mixed-precision multigrid levels)
   double* d_cache = nullptr;
   double* d_ubar = nullptr;
 };
@@ -116,6 +117,54 @@ static cudaError_t update_cell_flags(hf_space* sp, cudaStream_t s) {
   const long long n = sp->lat.n_el * (sp->dim == 3 ? sp->n1 * sp->n1 : sp->n1);
   k_line_masks<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sp->lat, sp->dim, sp->degree, sp->d_mask, sp->d_lmask);
   return cudaGetLastError();
+}
+
+// mode: 0 plain, 1 zero constrained outputs, 2 add into out with constrained dropped.
+// Input/output element types may differ (the boundary of fp32 multigrid
+// levels); intermediate passes and all arithmetic are fp64.
+template <typename TI, typename TO>
+static int transfer_run(hf_transfer* t, bool prolong, const TI* in, TO* out, int mode, cudaStream_t s) {
+  const hf_space* src = prolong ? t->coarse : t->fine;
+  const hf_space* dst = prolong ? t->fine : t->coarse;
+  int dim = src->dim, C = dim;
+  int n[3] = {src->lat.nodes[0], src->lat.nodes[1], dim == 3 ? src->lat.nodes[2] : 1};
+  const double* cur = nullptr;
+  for (int a = 0; a < dim; ++a) {
+    bool last = (a == dim - 1);
+    int nout = dst->lat.nodes[a];
+    long long total;
+    if (a == 0) total = (long long)C * nout * n[1] * n[2];
+    else if (a == 1) total = (long long)C * n[0] * nout * n[2];
+    else total = (long long)C * n[0] * n[1] * nout;
+    const int* rp = prolong ? t->d_pp[a] : t->d_rp[a];
+    const int* cl = prolong ? t->d_pc[a] : t->d_rc[a];
+    const double* w = prolong ? t->d_pw[a] : t->d_rw[a];
+    double* tmp = t->d_tmp[a & 1];
+    const unsigned blocks = vec_blocks(total);
+    if (a == 0 && last) {
+      k_axis<TI, TO><<<blocks, 256, 0, s>>>(in, out, n[0], n[1], n[2], C, a, nout, rp, cl, w, dst->d_mask, mode);
+    } else if (a == 0) {
+      k_axis<TI, double><<<blocks, 256, 0, s>>>(in, tmp, n[0], n[1], n[2], C, a, nout, rp, cl, w, dst->d_mask, 0);
+    } else if (last) {
+      k_axis<double, TO><<<blocks, 256, 0, s>>>(cur, out, n[0], n[1], n[2], C, a, nout, rp, cl, w, dst->d_mask, mode);
+    } else {
+      k_axis<double, double><<<blocks, 256, 0, s>>>(cur, tmp, n[0], n[1], n[2], C, a, nout, rp, cl, w, dst->d_mask, 0);
+    }
+    HF_CUDA(cudaGetLastError());
+    n[a] = nout;
+    cur = tmp;
+  }
+  return HF_OK;
+}
+
+static int transfer_dispatch(hf_transfer* t, bool prolong, const void* in, int in_bits, void* out, int out_bits,
+                             int mode, cudaStream_t s) {
+  if ((in_bits != 32 && in_bits != 64) || (out_bits != 32 && out_bits != 64)) return fail(HF_ERR_ARG, "bits: 32|64");
+  if (in_bits == 64 && out_bits == 64)
+    return transfer_run(t, prolong, (const double*)in, (double*)out, mode, s);
+  if (in_bits == 64) return transfer_run(t, prolong, (const double*)in, (float*)out, mode, s);
+  if (out_bits == 64) return transfer_run(t, prolong, (const float*)in, (double*)out, mode, s);
+  return transfer_run(t, prolong, (const float*)in, (float*)out, mode, s);
 }
 
 extern "C" {
@@ -345,18 +394,21 @@ HF_API int hf_jacobian_range(hf_space* sp, const double* u_dev, void* stream, do
   return HF_OK;
 }
 
-HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev, void* stream, hf_tangent** out,
-                             hf_error_info* err) {
+HF_API int hf_tangent_create_ex(hf_space* sp, int strategy, int storage_bits, const double* ubar_dev, void* stream,
+                                hf_tangent** out, hf_error_info* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (!sp || !ubar_dev || !out) return fail(HF_ERR_ARG, "null argument");
   if (strategy < HF_SCALAR || strategy > HF_TENSOR4) return fail(HF_ERR_ARG, "unknown strategy");
+  if (storage_bits != 32 && storage_bits != 64) return fail(HF_ERR_ARG, "storage_bits must be 32 or 64");
   cudaStream_t s = S(stream);
   hf_tangent* op = new hf_tangent();
   op->sp = sp;
   op->strategy = strategy;
   op->nf = nfields(sp->dim, strategy);
-  const long long ncache = tile_cache_doubles(sp->dim, sp->n1, op->nf, sp->lat.n_el);
-  HF_CUDA(cudaMalloc((void**)&op->d_cache, sizeof(double) * (ncache > 0 ? ncache : 1)));
+  op->fp32 = storage_bits == 32;
+  const int esz = op->fp32 ? 4 : 8;
+  const long long ncache = tile_cache_doubles(sp->dim, sp->n1, op->nf, sp->lat.n_el, esz);
+  HF_CUDA(cudaMalloc((void**)&op->d_cache, (size_t)esz * (ncache > 0 ? ncache : 1)));
   if (strategy == HF_SCALAR) {
     HF_CUDA(cudaMalloc((void**)&op->d_ubar, sizeof(double) * sp->n_dofs));
     HF_CUDA(cudaMemcpyAsync(op->d_ubar, ubar_dev, sizeof(double) * sp->n_dofs, cudaMemcpyDeviceToDevice, s));
@@ -367,6 +419,7 @@ HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev,
   a.x = ubar_dev;
   a.cache_out = op->d_cache;
   a.detmin = sp->d_u64;
+  a.fp32 = op->fp32;
   HF_CUDA(cell(sp, OP_BUILD, strategy, a, s));
   unsigned long long o;
   HF_CUDA(cudaMemcpyAsync(&o, sp->d_u64, sizeof(o), cudaMemcpyDeviceToHost, s));
@@ -379,12 +432,18 @@ HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev,
   return HF_OK;
 }
 
+HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev, void* stream, hf_tangent** out,
+                             hf_error_info* err) {
+  return hf_tangent_create_ex(sp, strategy, 64, ubar_dev, stream, out, err);
+}
+
 static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev, int fill,
                          void* stream, long long tile0 = 0, long long tile1 = -1) {
   if (!op || !x_dev || !y_dev) return fail(HF_ERR_ARG, "null argument");
   CellArgs a = base_args(op->sp);
   a.tile0 = tile0;
   a.tile1 = tile1;
+  a.fp32 = op->fp32;
   a.x = x_dev;
   a.y = y_dev;
   a.cache = op->d_cache;
@@ -410,8 +469,12 @@ HF_API int hf_tangent_apply_flagged(hf_tangent* op, const double* x_dev, double*
     const char* e = std::getenv("HF_PDL");
     pdl = e ? std::atoi(e) : 1;
   }
-  k_fill_masked<<<vec_blocks(op->sp->n_dofs), 256, 0, S(stream)>>>(op->sp->n_dofs, y_dev, x_dev, op->sp->d_mask, 0.0,
-                                                                   skip_dev);
+  if (op->fp32)
+    k_fill_masked<float><<<vec_blocks(op->sp->n_dofs), 256, 0, S(stream)>>>(
+        op->sp->n_dofs, (float*)y_dev, (const float*)x_dev, op->sp->d_mask, 0.0, skip_dev);
+  else
+    k_fill_masked<<<vec_blocks(op->sp->n_dofs), 256, 0, S(stream)>>>(op->sp->n_dofs, y_dev, x_dev, op->sp->d_mask,
+                                                                     0.0, skip_dev);
   HF_CUDA(cudaGetLastError());
   if (op->sp->lat.n_el == 0) return HF_OK;
   return tangent_apply(op, x_dev, y_dev, skip_dev, pdl, stream);
@@ -448,7 +511,8 @@ HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, 
 
 HF_API int hf_tangent_assemble_local(hf_tangent* op, double* vals_dev, void* stream) {
   if (!op || !vals_dev) return fail(HF_ERR_ARG, "null argument");
-  if (op->strategy != HF_TENSOR4) return fail(HF_ERR_ARG, "element matrices are formed from a tensor4 cache");
+  if (op->strategy != HF_TENSOR4 || op->fp32)
+    return fail(HF_ERR_ARG, "element matrices are formed from an fp64 tensor4 cache");
   const hf_space* sp = op->sp;
   if ((sp->dim == 3 && sp->n1 > 3) || (sp->dim == 2 && sp->n1 > 5))
     return fail(HF_ERR_UNSUPPORTED, "matrix-based assembly is instantiated for 3D Q1-Q2 and 2D Q1-Q4");
@@ -466,9 +530,10 @@ HF_API int hf_space_cell_dofs(const hf_space* sp, long long* dofs_dev, void* str
 
 HF_API int hf_tangent_diagonal(hf_tangent* op, double* d_dev, void* stream) {
   if (!op || !d_dev) return fail(HF_ERR_ARG, "null argument");
+  if (op->fp32) return fail(HF_ERR_UNSUPPORTED, "diagonal of an fp32-storage tangent: use the fp64 operator");
   const hf_space* sp = op->sp;
   cudaStream_t s = S(stream);
-  k_fill_masked<<<vec_blocks(sp->n_dofs), 256, 0, s>>>(sp->n_dofs, d_dev, nullptr, sp->d_mask, 1.0, nullptr);
+  k_fill_masked<double><<<vec_blocks(sp->n_dofs), 256, 0, s>>>(sp->n_dofs, d_dev, nullptr, sp->d_mask, 1.0, nullptr);
   HF_CUDA(cudaGetLastError());
   CellArgs a = base_args(sp);
   a.y = d_dev;
@@ -486,7 +551,7 @@ HF_API int hf_tangent_storage(const hf_tangent* op, long long* storage_bytes, in
   int payload = op->strategy == HF_SCALAR ? 1 : (op->strategy == HF_TENSOR2 ? 2 + nv : nv + nv * (nv + 1) / 2);
   long long nqp = sp->lat.n_qp;
   if (payload_scalars) *payload_scalars = payload;
-  if (payload_bytes) *payload_bytes = 8ll * payload * nqp;
+  if (payload_bytes) *payload_bytes = (op->fp32 ? 4ll : 8ll) * payload * nqp;
   // operators.py:412-417: payload + (jac_inv or jac_spatial_inv) + jxw
   if (storage_bytes) *storage_bytes = 8ll * nqp * (payload + d * d + 1);
   return HF_OK;
@@ -600,39 +665,25 @@ HF_API int hf_transfer_create(const hf_space* coarse, const hf_space* fine, cons
   return HF_OK;
 }
 
-// mode: 0 plain, 1 zero constrained outputs, 2 add into out with constrained dropped
-static int transfer_run(hf_transfer* t, bool prolong, const double* in, double* out, int mode, cudaStream_t s) {
-  const hf_space* src = prolong ? t->coarse : t->fine;
-  const hf_space* dst = prolong ? t->fine : t->coarse;
-  int dim = src->dim, C = dim;
-  int n[3] = {src->lat.nodes[0], src->lat.nodes[1], dim == 3 ? src->lat.nodes[2] : 1};
-  const double* cur = in;
-  for (int a = 0; a < dim; ++a) {
-    bool last = (a == dim - 1);
-    double* dst_buf = last ? out : t->d_tmp[a & 1];
-    int nout = dst->lat.nodes[a];
-    long long total = (long long)C * nout * (a == 0 ? 1 : n[0]) * (a == 1 ? 1 : n[1]) * (a == 2 ? 1 : n[2]);
-    if (a == 0) total = (long long)C * nout * n[1] * n[2];
-    else if (a == 1) total = (long long)C * n[0] * nout * n[2];
-    else total = (long long)C * n[0] * n[1] * nout;
-    k_axis<<<vec_blocks(total), 256, 0, s>>>(cur, dst_buf, n[0], n[1], n[2], C, a, nout,
-                                             prolong ? t->d_pp[a] : t->d_rp[a], prolong ? t->d_pc[a] : t->d_rc[a],
-                                             prolong ? t->d_pw[a] : t->d_rw[a], dst->d_mask, last ? mode : 0);
-    HF_CUDA(cudaGetLastError());
-    n[a] = nout;
-    cur = dst_buf;
-  }
-  return HF_OK;
-}
-
 HF_API int hf_prolong(hf_transfer* t, const double* xc, double* xf, int mode, void* stream) {
   if (!t || !xc || !xf) return fail(HF_ERR_ARG, "null argument");
-  return transfer_run(t, true, xc, xf, mode, S(stream));
+  return transfer_dispatch(t, true, xc, 64, xf, 64, mode, S(stream));
 }
 
 HF_API int hf_restrict(hf_transfer* t, const double* rf, double* rc, int mode, void* stream) {
   if (!t || !rf || !rc) return fail(HF_ERR_ARG, "null argument");
-  return transfer_run(t, false, rf, rc, mode, S(stream));
+  return transfer_dispatch(t, false, rf, 64, rc, 64, mode, S(stream));
+}
+
+HF_API int hf_prolong_ex(hf_transfer* t, const void* xc, int in_bits, void* xf, int out_bits, int mode, void* stream) {
+  if (!t || !xc || !xf) return fail(HF_ERR_ARG, "null argument");
+  return transfer_dispatch(t, true, xc, in_bits, xf, out_bits, mode, S(stream));
+}
+
+HF_API int hf_restrict_ex(hf_transfer* t, const void* rf, int in_bits, void* rc, int out_bits, int mode,
+                          void* stream) {
+  if (!t || !rf || !rc) return fail(HF_ERR_ARG, "null argument");
+  return transfer_dispatch(t, false, rf, in_bits, rc, out_bits, mode, S(stream));
 }
 
 HF_API int hf_transfer_destroy(hf_transfer* t) {
@@ -706,6 +757,51 @@ HF_API int hf_probe_dfma(long long iters, int blocks, int threads, double* sink_
   return HF_OK;
 }
 
+// ---- fp32 vector algebra of mixed-precision multigrid levels (arithmetic in fp64)
+HF_API int hf_fill_masked_f32(long long n, float* y, const float* x, const unsigned char* mask, double masked_value,
+                              void* stream) {
+  if (!y || !mask) return fail(HF_ERR_ARG, "null argument");
+  k_fill_masked<float><<<vec_blocks(n), 256, 0, S(stream)>>>(n, y, x, mask, masked_value, nullptr);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_cheb_step_f32(long long n, float* x, float* d, const float* b, const float* ax, const float* inv_d,
+                            int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
+                            const unsigned char* fill_mask, float* y_next, void* stream) {
+  if (!x || !d || !b || !inv_d) return fail(HF_ERR_ARG, "null argument");
+  k_cheb<float><<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev,
+                                                      fill_mask, y_next);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_resid_masked_f32(long long n, float* r, const float* b, const float* ax, const unsigned char* mask,
+                               void* stream) {
+  if (!r || !b || !ax || !mask) return fail(HF_ERR_ARG, "null argument");
+  k_resid_masked<float><<<vec_blocks(n), 256, 0, S(stream)>>>(n, r, b, ax, mask);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_dot_f32(hf_ws* w, long long n, const float* a, const float* b, double* out_dev, void* stream) {
+  if (!w || !a || !b || !out_dev) return fail(HF_ERR_ARG, "null argument");
+  k_dot<float><<<red_blocks(n), RED_THREADS, 0, S(stream)>>>(n, a, b, w->d_partials, w->d_counter, out_dev, nullptr);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_resnorm_check_f32(hf_ws* w, long long n, const float* b, const float* ax, double* scal, int out_idx,
+                                int target_idx, int* flag_dev, void* stream) {
+  if (!w || !b || !ax || !scal || !flag_dev) return fail(HF_ERR_ARG, "null argument");
+  cudaStream_t s = S(stream);
+  k_resnorm_check<float><<<red_blocks(n), RED_THREADS, 0, s>>>(n, b, ax, w->d_partials, w->d_counter, scal, out_idx,
+                                                                target_idx, flag_dev);
+  k_scalar<<<1, 32, 0, s>>>(0, scal, out_idx, target_idx, 0.0, flag_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
 HF_API int hf_halo_add(long long n, double* y, const double* recv, const unsigned char* mask, void* stream) {
   if (!y || !recv || !mask) return fail(HF_ERR_ARG, "null argument");
   if (n <= 0) return HF_OK;
@@ -718,8 +814,8 @@ HF_API int hf_cheb_step(long long n, double* x, double* d, const double* b, cons
                         int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
                         void* stream) {
   if (!x || !d || !b || !inv_d) return fail(HF_ERR_ARG, "null argument");
-  k_cheb<<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev,
-                                               nullptr, nullptr);
+  k_cheb<double><<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev,
+                                                       nullptr, nullptr);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }
@@ -728,8 +824,8 @@ HF_API int hf_cheb_step_fill(long long n, double* x, double* d, const double* b,
                              int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
                              const unsigned char* mask, double* y_next, void* stream) {
   if (!x || !d || !b || !inv_d || !mask || !y_next) return fail(HF_ERR_ARG, "null argument");
-  k_cheb<<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev, mask,
-                                               y_next);
+  k_cheb<double><<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev,
+                                                       mask, y_next);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }

@@ -66,6 +66,7 @@ struct CellArgs {
   const uint32_t* lmask;    // [n_el * lines] constraint bits per last-axis line (k_line_masks)
   const int* skip;          // optional device flag; non-zero -> kernel is a no-op
   int fill;                 // apply: 0 plain, 1/2 PDL secondary (hf_line.cuh LineArgs::fill)
+  int fp32;                 // apply/build: cache and x/y stored as float (mixed-precision levels)
   long long tile0, tile1;   // apply: tile range; tile1 < 0 means all tiles
   unsigned long long* detmin;  // ordered-double min of det F (build / residual / range)
   unsigned long long* detmax;
@@ -409,7 +410,7 @@ HF_DEV void gather_nodal(const double* __restrict__ v, const uint8_t* __restrict
 // ---------------------------------------------------------------------------
 // cache build (operators.py:292-311); also records min det F
 // ---------------------------------------------------------------------------
-template <int DIM, int N, int VAR>
+template <int DIM, int N, int VAR, typename ST = double>
 __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_build(const CellArgs a) {
   using K = Cfg<DIM, N>;
   constexpr int NQ = K::NQ;
@@ -437,8 +438,8 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_build(const CellArgs a) {
   if (!t.act) return;
   constexpr int NF = CacheFields<DIM, VAR>::NF;
   using TL = TileLayout<DIM, N>;
-  double* o = a.cache_out;
-  auto put = [&](int f, double v) { o[TL::index(t.e, t.lq, f, NF)] = v; };
+  ST* o = reinterpret_cast<ST*>(a.cache_out);  // fp64, or fp32 storage of a mixed-precision level
+  auto put = [&](int f, double v) { o[TL::template index_e<sizeof(ST)>(t.e, t.lq, f, NF)] = (ST)v; };
   int f = 0;
   if (VAR == SCALAR) {
     put(f++, k.c1);

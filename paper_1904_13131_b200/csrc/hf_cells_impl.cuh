@@ -8,17 +8,17 @@ namespace hf {
 
 // Launch of the line-parallel apply (hf_line.cuh): persistent warps, grid
 // sized to the resident capacity (148 SMs x blocks per SM) or the tile count.
-template <int DIM, int N, int VAR>
-cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
+template <int DIM, int N, int VAR, typename ST>
+cudaError_t launch_apply_line_t(const CellArgs& c, cudaStream_t s) {
   using K = LineCfg<DIM, N>;
-  using PL = LinePlan<DIM, N, VAR>;
+  using PL = LinePlan<DIM, N, VAR, ST>;
   static int resident = -1;
   if (resident < 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_apply_line<DIM, N, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_apply_line<DIM, N, VAR, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)PL::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0, dev = 0, nsm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_line<DIM, N, VAR>, PL::NT, PL::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_line<DIM, N, VAR, ST>, PL::NT, PL::SMEM);
     if (e != cudaSuccess) return e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -51,7 +51,7 @@ cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
   if (nb > resident) nb = resident;
   if (nb <= 0) return cudaSuccess;
   if (!c.fill) {
-    k_apply_line<DIM, N, VAR><<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);
+    k_apply_line<DIM, N, VAR, ST><<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);
     return cudaGetLastError();
   }
   // programmatic dependent launch after the fill kernel (hf_api.cu)
@@ -65,7 +65,12 @@ cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_apply_line<DIM, N, VAR>, a, T);
+  return cudaLaunchKernelEx(&cfg, k_apply_line<DIM, N, VAR, ST>, a, T);
+}
+
+template <int DIM, int N, int VAR>
+cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
+  return c.fp32 ? launch_apply_line_t<DIM, N, VAR, float>(c, s) : launch_apply_line_t<DIM, N, VAR, double>(c, s);
 }
 
 template <int DIM, int N>
@@ -82,9 +87,15 @@ cudaError_t launch_one(int op, int var, const CellArgs& a, int mode, double targ
       if (var == TENSOR2) return launch_apply_line<DIM, N, TENSOR2>(a, s);
       return launch_apply_line<DIM, N, TENSOR4>(a, s);
     case OP_BUILD:
-      if (var == SCALAR) k_build<DIM, N, SCALAR><<<grid, block, sm, s>>>(a);
-      else if (var == TENSOR2) k_build<DIM, N, TENSOR2><<<grid, block, sm, s>>>(a);
-      else k_build<DIM, N, TENSOR4><<<grid, block, sm, s>>>(a);
+      if (a.fp32) {
+        if (var == SCALAR) k_build<DIM, N, SCALAR, float><<<grid, block, sm, s>>>(a);
+        else if (var == TENSOR2) k_build<DIM, N, TENSOR2, float><<<grid, block, sm, s>>>(a);
+        else k_build<DIM, N, TENSOR4, float><<<grid, block, sm, s>>>(a);
+      } else {
+        if (var == SCALAR) k_build<DIM, N, SCALAR><<<grid, block, sm, s>>>(a);
+        else if (var == TENSOR2) k_build<DIM, N, TENSOR2><<<grid, block, sm, s>>>(a);
+        else k_build<DIM, N, TENSOR4><<<grid, block, sm, s>>>(a);
+      }
       break;
     case OP_DIAG:
       if (var == SCALAR) k_diag<DIM, N, SCALAR><<<grid, block, sm, s>>>(a);

@@ -128,7 +128,12 @@ struct LineCfg {
 template <int DIM, int N>
 struct TileLayout {
   using K = LineCfg<DIM, N>;
-  HF_DEV static constexpr long long chunk(int nf) { return ((long long)nf * K::LANES + 1) & ~1ll; }
+  // elements per chunk for ESZ-byte elements, rounded to 16 bytes
+  template <int ESZ = 8>
+  HF_DEV static constexpr long long chunk_e(int nf) {
+    return ((long long)nf * K::LANES + (16 / ESZ - 1)) & ~(long long)(16 / ESZ - 1);
+  }
+  HF_DEV static constexpr long long chunk(int nf) { return chunk_e<8>(nf); }
   HF_DEV static constexpr long long stride(int nf) { return N * chunk(nf); }
   // flat index of field f of (cell e, local q-point lq, x fastest)
   HF_DEV static long long index(long long e, int lq, int f, int nf) {
@@ -137,12 +142,21 @@ struct TileLayout {
     const int iq = lq % N, line = lq / N;
     return tile * stride(nf) + iq * chunk(nf) + (long long)f * K::LANES + m * K::L + line;
   }
+  // same for ESZ-byte elements (the fp32 storage of mixed-precision levels)
+  template <int ESZ>
+  HF_DEV static long long index_e(long long e, int lq, int f, int nf) {
+    const long long tile = e / K::CPW;
+    const int m = (int)(e - tile * K::CPW);
+    const int iq = lq % N, line = lq / N;
+    return tile * (N * chunk_e<ESZ>(nf)) + iq * chunk_e<ESZ>(nf) + (long long)f * K::LANES + m * K::L + line;
+  }
 };
-inline long long tile_cache_doubles(int dim, int n1, int nf, long long n_el) {
+inline long long tile_cache_doubles(int dim, int n1, int nf, long long n_el, int esz = 8) {
   int nq = dim == 2 ? n1 * n1 : n1 * n1 * n1;
   int lanes = (32 / (nq / n1)) * (nq / n1);
   int cpw = 32 / (nq / n1);
   long long tiles = (n_el + cpw - 1) / cpw;
-  long long ch = ((long long)nf * lanes + 1) & ~1ll;
-  return tiles * n1 * ch;
+  const long long r = 16 / esz - 1;
+  long long ch = ((long long)nf * lanes + r) & ~r;
+  return tiles * n1 * ch;  // elements of esz bytes
 }

@@ -169,7 +169,7 @@ HF_DEV void last_axis_line(const HfLattice& lat, long long node0, int t, long lo
 // one tile deep): nodal values of x (and ubar for the scalar strategy) and the
 // line's constraint bits (bit c*N + l).
 template <int DIM, int N, int VAR>
-struct Gather {
+struct Gather {  // values held in fp64 whatever the storage type
   double u[DIM][N];
   double ub[DIM][N];  // scalar strategy only
   unsigned mb;
@@ -177,10 +177,11 @@ struct Gather {
   bool live;
 };
 
-template <int DIM, int N, int VAR>
+template <int DIM, int N, int VAR, typename ST = double>
 HF_DEV void gather_tile(const LineArgs& a, long long tile, long long ntiles, int m, int t, bool act,
                         Gather<DIM, N, VAR>& g) {
   using K = LineCfg<DIM, N>;
+  const ST* xs = reinterpret_cast<const ST*>(a.x);  // fp64, or fp32 vectors of a mixed-precision level
   g.e = tile * K::CPW + m;
   g.live = act && tile < ntiles && g.e < a.lat.n_el;
   g.mb = 0;
@@ -193,7 +194,7 @@ HF_DEV void gather_tile(const LineArgs& a, long long tile, long long ntiles, int
     const long long d0 = (nb + l * s_last) * DIM;
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
-      g.u[c][l] = __ldg(a.x + d0 + c);
+      g.u[c][l] = (double)__ldg(xs + d0 + c);
       if (VAR == SCALAR) g.ub[c][l] = __ldg(a.ubar + d0 + c);
     }
   }
@@ -286,15 +287,16 @@ HF_DEV void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned lon
 
 // shared-memory plan of one block of W warps, each with NB line buffers and a
 // private ring of RW cache stages
-template <int DIM, int N, int VAR>
+template <int DIM, int N, int VAR, typename ST = double>
 struct LinePlan {
   using K = LineCfg<DIM, N>;
   static constexpr int NB = (VAR == SCALAR) ? 5 : 3;
   static constexpr int NF = (VAR == SCALAR) ? 2 + DIM * DIM : CacheFields<DIM, VAR>::NF;
-  static constexpr long long CH = TileLayout<DIM, N>::chunk(NF);  // doubles per (tile, iq) chunk
+  // ST elements per (tile, iq) chunk (fp64, or the fp32 storage of a mixed-precision level)
+  static constexpr long long CH = TileLayout<DIM, N>::template chunk_e<sizeof(ST)>(NF);
   static constexpr size_t BUDGET = 226 * 1024;
   static constexpr size_t perw(int rw) {
-    return sizeof(double) * ((size_t)rw * CH + (size_t)NB * LineLay<DIM, N>::BUF) + 16 * rw;
+    return sizeof(ST) * (size_t)rw * CH + sizeof(double) * (size_t)NB * LineLay<DIM, N>::BUF + 16 * rw;
   }
   // RW = min(N, 3) stages: at Q2 the chunks of the next tile are issued while
   // the current tile's point phase consumes its own, one tile period ahead of
@@ -310,10 +312,11 @@ struct LinePlan {
   static constexpr size_t SMEM = (size_t)W * perw(RW);
 };
 
-template <int DIM, int N, int VAR>
-__global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(const LineArgs a, const TabLine<N> T) {
+template <int DIM, int N, int VAR, typename ST = double>
+__global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
+    k_apply_line(const LineArgs a, const TabLine<N> T) {
   using K = LineCfg<DIM, N>;
-  using PL = LinePlan<DIM, N, VAR>;
+  using PL = LinePlan<DIM, N, VAR, ST>;
   using Y = LineLay<DIM, N>;
   constexpr int NF = PL::NF;
   constexpr int NB = PL::NB;
@@ -325,8 +328,9 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
   if (a.skip && *a.skip) return;
   extern __shared__ __align__(128) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* ring = smem + (size_t)warp * RW * CH;  // this warp's stages (16-byte aligned)
-  double* lbuf = smem + (size_t)W * RW * CH;      // W x NB x BUF
+  ST* ring = reinterpret_cast<ST*>(smem) + (size_t)warp * RW * CH;  // this warp's stages (16-byte aligned)
+  double* lbuf = reinterpret_cast<double*>(reinterpret_cast<ST*>(smem) + (size_t)W * RW * CH);  // W x NB x BUF
+  const ST* cache = reinterpret_cast<const ST*>(a.cache);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(lbuf + (size_t)W * NB * Y::BUF) + warp * RW;
   const long long ntiles = a.tile1;  // tiles [a.tile0, a.tile1) of the (CPW-cell) tiling
   const long long tstride = (long long)N * CH;
@@ -335,9 +339,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
     const long long tile = a.tile0 + blockIdx.x + (warp + (j / N) * W) * (long long)gridDim.x;
     if (tile >= ntiles) return;
     const int s = (int)(j % RW);
-    mbar_expect_tx(full + s, (unsigned)(CH * sizeof(double)));
-    tma_load_1d(ring + (size_t)s * CH, a.cache + tile * tstride + (j % N) * CH, (unsigned)(CH * sizeof(double)),
-                full + s);
+    mbar_expect_tx(full + s, (unsigned)(CH * sizeof(ST)));
+    tma_load_1d(ring + (size_t)s * CH, cache + tile * tstride + (j % N) * CH, (unsigned)(CH * sizeof(ST)), full + s);
   };
   if (lane == 0) {
     for (int s = 0; s < RW; ++s) mbar_init(full + s, 1);
@@ -367,10 +370,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
   long long jc = 0;  // this warp's chunk counter
   const long long tstep = (long long)W * gridDim.x;
   Gather<DIM, N, VAR> nxt;
-  gather_tile<DIM, N, VAR>(a, a.tile0 + blockIdx.x + (long long)warp * gridDim.x, ntiles, m, t, act, nxt);
+  gather_tile<DIM, N, VAR, ST>(a, a.tile0 + blockIdx.x + (long long)warp * gridDim.x, ntiles, m, t, act, nxt);
   for (long long tile = a.tile0 + blockIdx.x + (long long)warp * gridDim.x; tile < ntiles; tile += tstep) {
     const Gather<DIM, N, VAR> g = nxt;
-    gather_tile<DIM, N, VAR>(a, tile + tstep, ntiles, m, t, act, nxt);  // in flight during this tile
+    gather_tile<DIM, N, VAR, ST>(a, tile + tstep, ntiles, m, t, act, nxt);  // in flight during this tile
     const long long e = g.e;
     const bool live = g.live;
     double u[DIM][N];
@@ -392,12 +395,12 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
     }
     const int pt0 = lbase<DIM, N, 0>(t);
     // one Gauss point of this thread's x-line from its cache chunk
-    auto point = [&](const int iq, const double* st) {
+    auto point = [&](const int iq, const ST* st) {
       if (live) {
       const int pt = pt0 + iq;
       double f[NF];
 #pragma unroll
-      for (int q = 0; q < NF; ++q) f[q] = st[q * K::LANES];
+      for (int q = 0; q < NF; ++q) f[q] = (double)st[q * K::LANES];
       double gu[DIM][DIM];
 #pragma unroll
       for (int cc = 0; cc < DIM; ++cc) {
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR>::NT, 1) k_apply_line(con
         const long long d0 = (nb + l * s_last) * DIM;
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc)
-          if (!((g.mb >> (cc * N + l)) & 1u)) atomicAdd(a.y + d0 + cc, v[cc][l]);
+          if (!((g.mb >> (cc * N + l)) & 1u)) atomicAdd(reinterpret_cast<ST*>(a.y) + d0 + cc, (ST)v[cc][l]);
       }
     }
     __syncwarp();  // line buffers are reused by the next tile

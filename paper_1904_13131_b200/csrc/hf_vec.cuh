@@ -80,22 +80,24 @@ inline unsigned red_blocks(long long n) {
   return (unsigned)b;
 }
 
-__global__ void k_dot(long long n, const double* __restrict__ a, const double* __restrict__ b, double* partials,
+template <typename T = double>
+__global__ void k_dot(long long n, const T* __restrict__ a, const T* __restrict__ b, double* partials,
                       unsigned* counter, double* out, const int* skip) {
   if (skip && *skip) return;
   double s = 0.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    s = fma(a[i], b[i], s);
+    s = fma((double)a[i], (double)b[i], s);
   grid_reduce(s, partials, counter, out);
 }
 
 // y[i] = mask[i] ? (x ? x[i] : mval) : 0
-__global__ void k_fill_masked(long long n, double* __restrict__ y, const double* __restrict__ x,
+template <typename T = double>
+__global__ void k_fill_masked(long long n, T* __restrict__ y, const T* __restrict__ x,
                               const uint8_t* __restrict__ mask, double mval, const int* skip) {
   asm volatile("griddepcontrol.launch_dependents;");  // a PDL secondary (the apply) may start now
   if (skip && *skip) return;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    y[i] = mask[i] ? (x ? x[i] : mval) : 0.0;
+    y[i] = mask[i] ? (x ? x[i] : (T)mval) : (T)0;
 }
 
 // Chebyshev step (multigrid.py:176-205, 280-296):
@@ -105,36 +107,38 @@ __global__ void k_fill_masked(long long n, double* __restrict__ y, const double*
 //   fill_mask != null: also y_next = mask ? x_new : 0, the initialisation of
 //   the NEXT tangent apply (which is launched as this kernel's programmatic
 //   dependent and skips its own fill); y_next may alias ax (read first)
-__global__ void k_cheb(long long n, double* __restrict__ x, double* __restrict__ d, const double* __restrict__ b,
-                       const double* ax, const double* __restrict__ inv_d, int first, double theta, double cd,
-                       double cz, int x_zero, const int* skip, const uint8_t* __restrict__ fill_mask,
-                       double* y_next) {
+template <typename T = double>
+__global__ void k_cheb(long long n, T* __restrict__ x, T* __restrict__ d, const T* __restrict__ b, const T* ax,
+                       const T* __restrict__ inv_d, int first, double theta, double cd, double cz, int x_zero,
+                       const int* skip, const uint8_t* __restrict__ fill_mask, T* y_next) {
   asm volatile("griddepcontrol.launch_dependents;");
   if (skip && *skip) return;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double z = inv_d[i] * (b[i] - (ax ? ax[i] : 0.0));
-    double di = first ? z / theta : cd * d[i] + cz * z;
-    d[i] = di;
-    const double xn = x_zero ? di : x[i] + di;
+    double z = (double)inv_d[i] * ((double)b[i] - (ax ? (double)ax[i] : 0.0));
+    double di = first ? z / theta : cd * (double)d[i] + cz * z;
+    d[i] = (T)di;
+    const T xn = (T)(x_zero ? di : (double)x[i] + di);
     x[i] = xn;
-    if (fill_mask) y_next[i] = fill_mask[i] ? xn : 0.0;
+    if (fill_mask) y_next[i] = fill_mask[i] ? xn : (T)0;
   }
 }
 
 // r = b - ax, r[mask] = 0
-__global__ void k_resid_masked(long long n, double* __restrict__ r, const double* __restrict__ b,
-                               const double* __restrict__ ax, const uint8_t* __restrict__ mask) {
+template <typename T = double>
+__global__ void k_resid_masked(long long n, T* __restrict__ r, const T* __restrict__ b, const T* __restrict__ ax,
+                               const uint8_t* __restrict__ mask) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    r[i] = mask[i] ? 0.0 : b[i] - ax[i];
+    r[i] = mask[i] ? (T)0 : (T)((double)b[i] - (double)ax[i]);
 }
 
 // ||b - ax||^2 -> scal[out]; if sqrt(.) <= scal[tgt] set *flag (coarse_solve check)
-__global__ void k_resnorm_check(long long n, const double* __restrict__ b, const double* __restrict__ ax,
-                                double* partials, unsigned* counter, double* scal, int out, int tgt, int* flag) {
+template <typename T = double>
+__global__ void k_resnorm_check(long long n, const T* __restrict__ b, const T* __restrict__ ax, double* partials,
+                                unsigned* counter, double* scal, int out, int tgt, int* flag) {
   if (*flag) return;
   double s = 0.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double r = b[i] - ax[i];
+    double r = (double)b[i] - (double)ax[i];
     s = fma(r, r, s);
   }
   grid_reduce(s, partials, counter, scal + out);
@@ -211,8 +215,9 @@ __global__ void k_resid_finalize(long long n_nodes, int C, double* __restrict__ 
 // One axis of a tensor-product 1D operator on a (n2, n1, n0, C) lattice array
 // (multigrid.py:39-55).  Row o of the banded 1D matrix is (cols, w)[rowptr[o]..].
 // mode 0: out = v;  mode 1: out = mask ? 0 : v;  mode 2: out += mask ? 0 : v
-__global__ void k_axis(const double* __restrict__ in, double* __restrict__ out, int n0, int n1, int n2, int C,
-                       int axis, int nout, const int* __restrict__ rowptr, const int* __restrict__ cols,
+template <typename TI = double, typename TO = double>
+__global__ void k_axis(const TI* __restrict__ in, TO* __restrict__ out, int n0, int n1, int n2, int C, int axis,
+                       int nout, const int* __restrict__ rowptr, const int* __restrict__ cols,
                        const double* __restrict__ w, const uint8_t* __restrict__ mask, int mode) {
   int m0 = axis == 0 ? nout : n0, m1 = axis == 1 ? nout : n1, m2 = axis == 2 ? nout : n2;
   long long total = (long long)m0 * m1 * m2 * C;
@@ -228,10 +233,11 @@ __global__ void k_axis(const double* __restrict__ in, double* __restrict__ out, 
     int o = axis == 0 ? i0 : (axis == 1 ? i1 : i2);
     long long base = (((long long)(axis == 2 ? 0 : i2) * n1 + (axis == 1 ? 0 : i1)) * n0 + (axis == 0 ? 0 : i0)) * C + c;
     double s = 0.0;
-    for (int k = rowptr[o]; k < rowptr[o + 1]; ++k) s = fma(w[k], in[base + (long long)cols[k] * in_stride], s);
-    if (mode == 0) out[t] = s;
-    else if (mode == 1) out[t] = mask[t] ? 0.0 : s;
-    else if (!mask[t]) out[t] += s;
+    for (int k = rowptr[o]; k < rowptr[o + 1]; ++k)
+      s = fma(w[k], (double)in[base + (long long)cols[k] * in_stride], s);
+    if (mode == 0) out[t] = (TO)s;
+    else if (mode == 1) out[t] = mask[t] ? (TO)0 : (TO)s;
+    else if (!mask[t]) out[t] = (TO)((double)out[t] + s);
   }
 }
 

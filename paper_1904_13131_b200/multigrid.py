@@ -36,6 +36,10 @@ from .operators import MatrixFreeTangent, Problem
 log = logging.getLogger(__name__)
 
 
+def _bits(t: torch.Tensor) -> int:
+    return 32 if t.dtype == torch.float32 else 64
+
+
 def _apply_into(op, x, y, skip=None):
     if hasattr(op, "apply_into"):
         return op.apply_into(x, y, skip)
@@ -71,11 +75,12 @@ class TransferOperator:
             pass
 
     def prolong_into(self, xc, xf, mode: int = 0):
-        check(lib().hf_prolong(self._h, dv.ptr(xc), dv.ptr(xf), mode, dv.stream()))
+        """fp64 or fp32 vectors on either side (mixed-precision levels)."""
+        check(lib().hf_prolong_ex(self._h, dv.ptr(xc), _bits(xc), dv.ptr(xf), _bits(xf), mode, dv.stream()))
         return xf
 
     def restrict_into(self, rf, rc, mode: int = 0):
-        check(lib().hf_restrict(self._h, dv.ptr(rf), dv.ptr(rc), mode, dv.stream()))
+        check(lib().hf_restrict_ex(self._h, dv.ptr(rf), _bits(rf), dv.ptr(rc), _bits(rc), mode, dv.stream()))
         return rc
 
     def prolong(self, x_coarse):
@@ -228,7 +233,9 @@ def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings,
         fill = fuse and (k < n_upd or fill_last)
         args = (n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None if zero else dv.ptr(ax), dv.ptr(inv_d), first, th, cd, cz,
                 int(zero), None)
-        if fill:
+        if x.dtype == torch.float32:
+            check(L.hf_cheb_step_f32(*args, mask if fill else None, dv.ptr(ax) if fill else None, dv.stream()))
+        elif fill:
             check(L.hf_cheb_step_fill(*args, mask, dv.ptr(ax), dv.stream()))
         else:
             check(L.hf_cheb_step(*args, dv.stream()))
@@ -260,9 +267,14 @@ def chebyshev_apply(apply_fn, inv_diagonal, lam_max: float, b, x, settings: Cheb
 class LevelOperator:
     """Tangent of one level plus its smoother data (multigrid.py:208-252)."""
 
-    def __init__(self, problem: Problem, u_level, strategy: str, seed: int, level: int, is_coarsest: bool = False):
+    def __init__(self, problem: Problem, u_level, strategy: str, seed: int, level: int, is_coarsest: bool = False,
+                 precision: str = "fp64"):
+        """``precision="fp32"``: the diagonal and the Lanczos range come from the
+        fp64 tangent; the smoother then runs on an fp32-storage tangent with fp32
+        level vectors (half the bytes per application)."""
         self.level = level
         self.problem = problem
+        self.precision = precision
         try:
             self.op = MatrixFreeTangent(problem, u_level, strategy)
         except NonPositiveJacobian as err:
@@ -275,10 +287,17 @@ class LevelOperator:
             lo, _ = estimate_eigenvalue_range(self.op, self.diag, seed=seed, iterations=min(problem.n_dofs, 120),
                                               constrained=mask)
             self.lam_min = min(self.lam_min, lo)
+        dtype = torch.float64
+        if precision == "fp32":
+            self.op = MatrixFreeTangent(problem, u_level, strategy, storage="fp32")
+            self.inv_diag = self.inv_diag.float()
+            dtype = torch.float32
+        elif precision != "fp64":
+            raise ValueError(f"unknown precision {precision!r}")
         self._cap_warned = False
         n = problem.n_dofs
         # per-level V-cycle buffers
-        self.b = torch.zeros(n, dtype=torch.float64, device="cuda")
+        self.b = torch.zeros(n, dtype=dtype, device="cuda")
         self.x = torch.zeros_like(self.b)
         self.d = torch.zeros_like(self.b)
         self.ax = torch.zeros_like(self.b)
@@ -320,25 +339,35 @@ def _coarse_solve_into(level: LevelOperator, b, x, rel_target=1e-3, max_applicat
     L = lib()
     ws = dv.Workspace.get().handle
     scal, flag, d, ax = level.scal, level.flag, level.d, level.ax
+    f32 = x.dtype == torch.float32
+
+    def cheb(args, fill):
+        if f32:
+            check(L.hf_cheb_step_f32(*args, mask if fill else None, dv.ptr(ax) if fill else None, dv.stream()))
+        elif fill:
+            check(L.hf_cheb_step_fill(*args, mask, dv.ptr(ax), dv.stream()))
+        else:
+            check(L.hf_cheb_step(*args, dv.stream()))
+
     # scal[0] = ||b||^2, scal[1] = rel_target * ||b||, flag = (||b|| == 0)
-    dv.dot(b, b, scal[0:1])
+    if f32:
+        check(L.hf_dot_f32(ws, n, dv.ptr(b), dv.ptr(b), dv.ptr(scal[0:1]), dv.stream()))
+    else:
+        dv.dot(b, b, scal[0:1])
     check(L.hf_scalar_op(1, dv.ptr(scal), 0, 1, rel_target, dv.ptr(flag), dv.stream()))
     # x = 0 + inv_d b / theta; ax = mask ? x : 0 for the first application
     mask = level.problem.mask_ptr()
-    check(L.hf_cheb_step_fill(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None, dv.ptr(level.inv_diag), 1, theta, 0.0, 0.0, 1,
-                              None, mask, dv.ptr(ax), dv.stream()))
+    cheb((n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None, dv.ptr(level.inv_diag), 1, theta, 0.0, 0.0, 1, None), True)
     rho_old = 1.0 / sigma
     for step in range(2, max_applications + 1):
         level.op.apply_after_fill(x, ax, flag)
         if step % s.degree == 0:
-            check(L.hf_resnorm_check(ws, n, dv.ptr(b), dv.ptr(ax), dv.ptr(scal), 2, 1, dv.ptr(flag), dv.stream()))
+            rn = L.hf_resnorm_check_f32 if f32 else L.hf_resnorm_check
+            check(rn(ws, n, dv.ptr(b), dv.ptr(ax), dv.ptr(scal), 2, 1, dv.ptr(flag), dv.stream()))
         rho = 1.0 / (2.0 * sigma - rho_old)
         args = (n, dv.ptr(x), dv.ptr(d), dv.ptr(b), dv.ptr(ax), dv.ptr(level.inv_diag), 0, 0.0, rho * rho_old,
                 2.0 * rho / delta, 0, dv.ptr(flag))
-        if step < max_applications:  # the update also prepares the next application
-            check(L.hf_cheb_step_fill(*args, mask, dv.ptr(ax), dv.stream()))
-        else:
-            check(L.hf_cheb_step(*args, dv.stream()))
+        cheb(args, step < max_applications)  # the update also prepares the next application
         rho_old = rho
     return x
 
@@ -363,7 +392,8 @@ def _v_cycle_into(levels, transfers, b, x, lvl, steps, settings):
     C = levels[lvl - 1]
     filled = L.smooth_into(b, x, steps, settings, x_zero=True, fill_last=True)
     _apply_maybe_filled(L.op, x, L.ax, filled)
-    check(lib().hf_resid_masked(b.numel(), dv.ptr(L.r), dv.ptr(b), dv.ptr(L.ax), L.problem.mask_ptr(), dv.stream()))
+    rm = lib().hf_resid_masked_f32 if b.dtype == torch.float32 else lib().hf_resid_masked
+    check(rm(b.numel(), dv.ptr(L.r), dv.ptr(b), dv.ptr(L.ax), L.problem.mask_ptr(), dv.stream()))
     transfers[lvl - 1].restrict_into(L.r, C.b, mode=1)
     _v_cycle_into(levels, transfers, C.b, C.x, lvl - 1, steps, settings)
     transfers[lvl - 1].prolong_into(C.x, x, mode=2)
@@ -431,17 +461,22 @@ def build_transfers(problems):
     return [TransferOperator(problems[i], problems[i + 1]) for i in range(len(problems) - 1)]
 
 
-def build_level_operators(problems, u_fine, strategy: str = "tensor4", seed: int = 0, keep_constrained: bool = False):
-    """Linearise every level at the injected fine displacement (multigrid.py:358-369)."""
+def build_level_operators(problems, u_fine, strategy: str = "tensor4", seed: int = 0, keep_constrained: bool = False,
+                          coarse_precision: str = "fp64"):
+    """Linearise every level at the injected fine displacement (multigrid.py:358-369);
+    ``coarse_precision="fp32"`` runs every level below the finest in fp32 storage."""
     u_levels = restrict_solution(problems, dv.as_dev(u_fine), keep_constrained)
-    return [LevelOperator(p, u, strategy, seed=seed + 7919 * lvl, level=lvl, is_coarsest=(lvl == 0))
+    top = len(problems) - 1
+    return [LevelOperator(p, u, strategy, seed=seed + 7919 * lvl, level=lvl, is_coarsest=(lvl == 0),
+                          precision=coarse_precision if lvl < top else "fp64")
             for lvl, (p, u) in enumerate(zip(problems, u_levels))]
 
 
 def build_gmg(problems, u_fine, strategy: str = "tensor4", seed: int = 0, transfers=None,
-              keep_constrained: bool = False, use_graph: bool = True) -> GMGPreconditioner:
-    """(multigrid.py:372-382)"""
+              keep_constrained: bool = False, use_graph: bool = True,
+              coarse_precision: str = "fp64") -> GMGPreconditioner:
+    """(multigrid.py:372-382); ``coarse_precision="fp32"`` for the levels below the finest."""
     if transfers is None:
         transfers = build_transfers(problems)
-    levels = build_level_operators(problems, u_fine, strategy, seed, keep_constrained)
+    levels = build_level_operators(problems, u_fine, strategy, seed, keep_constrained, coarse_precision)
     return GMGPreconditioner(levels, transfers, use_graph=use_graph)

@@ -280,16 +280,23 @@ class CacheInfo:
 class MatrixFreeTangent:
     """Apply-only tangent backed by one of the three q-point caches (operators.py:319-417)."""
 
-    def __init__(self, problem: Problem, u_bar, strategy: str = "tensor4"):
+    def __init__(self, problem: Problem, u_bar, strategy: str = "tensor4", storage: str = "fp64"):
+        """``storage="fp32"`` keeps the q-point cache -- and the x / y vectors of
+        ``apply_into`` -- in float (mixed-precision multigrid levels, SURVEY §8(f)
+        row 1); all arithmetic stays fp64."""
         if strategy not in STRATEGIES:
             raise ValueError(f"unknown strategy {strategy!r}")
+        if storage not in ("fp64", "fp32"):
+            raise ValueError(f"unknown storage {storage!r}")
         self.problem = problem
         self.strategy = strategy
+        self.storage = storage
+        self.dtype = torch.float32 if storage == "fp32" else torch.float64
         ud = dv.as_dev(u_bar)
         h = ct.c_void_p()
         err = HfErrorInfo()
-        rc = lib().hf_tangent_create(problem._space, STRATEGY_CODE[strategy], dv.ptr(ud), dv.stream(), ct.byref(h),
-                                     ct.byref(err))
+        rc = lib().hf_tangent_create_ex(problem._space, STRATEGY_CODE[strategy], 32 if storage == "fp32" else 64,
+                                        dv.ptr(ud), dv.stream(), ct.byref(h), ct.byref(err))
         if rc == HF_ERR_JACOBIAN:
             _raise_jacobian(err)
         check(rc)
@@ -346,11 +353,16 @@ class MatrixFreeTangent:
         tensor in with a pinned ``out`` runs the host-to-host pipeline
         (``apply_host``)."""
         if (out is not None and isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned()
-                and out.is_pinned() and self.problem.mesh.n_elements >= 4096):
+                and out.is_pinned() and self.problem.mesh.n_elements >= 4096 and self.storage == "fp64"):
             return self.apply_host(x, out)
         xd = dv.as_dev(x)
-        y = torch.empty_like(xd)
-        self.apply_into(xd, y)
+        if self.storage == "fp32":  # the public apply stays fp64 in, fp64 out
+            y32 = torch.empty(xd.shape, dtype=torch.float32, device="cuda")
+            self.apply_into(xd.float(), y32)
+            y = y32.double()
+        else:
+            y = torch.empty_like(xd)
+            self.apply_into(xd, y)
         if out is not None:
             out.copy_(y, non_blocking=True)
             torch.cuda.current_stream().synchronize()
@@ -427,7 +439,7 @@ class MatrixFreeTangent:
         return self.apply(x)
 
     def diagonal(self, as_numpy: bool | None = None):
-        """diag(A), constrained entries 1 (operators.py:395-410)."""
+        """diag(A), constrained entries 1 (operators.py:395-410); fp64 storage only."""
         d = torch.empty(self.n_dofs, dtype=torch.float64, device="cuda")
         check(lib().hf_tangent_diagonal(self._op, dv.ptr(d), dv.stream()))
         return d.cpu().numpy() if as_numpy else d
@@ -469,10 +481,10 @@ class AssembledTangent:
         cols = torch.cat([cols[keep], fixed])
         vals = torch.cat([vals[keep], torch.ones(fixed.numel(), dtype=torch.float64, device="cuda")])
         n = problem.n_dofs
-        coo = torch.sparse_coo_tensor(torch.stack([rows, cols]), vals, (n, n), check_invariants=False).coalesce()
-        del rows, cols, vals, keep
         with warnings.catch_warnings():
-            warnings.simplefilter("ignore", UserWarning)  # "sparse CSR support is in beta"
+            warnings.simplefilter("ignore", UserWarning)  # torch: sparse invariant checks off / CSR "beta"
+            coo = torch.sparse_coo_tensor(torch.stack([rows, cols]), vals, (n, n), check_invariants=False).coalesce()
+            del rows, cols, vals, keep
             self.matrix = coo.to_sparse_csr()
         self._diag = None
 

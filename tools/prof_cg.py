@@ -35,7 +35,7 @@ else:
     b[fine.mask_dev] = 0.0
     keep = False
 op = MatrixFreeTangent(fine, u, "tensor4")
-gmg = build_gmg(probs, u, "tensor4", seed=0, keep_constrained=keep)
+gmg = build_gmg(probs, u, "tensor4", seed=0, keep_constrained=keep, coarse_precision=os.environ.get("HF_COARSE_PRECISION", "fp64"))
 cg(op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=2)  # warm-up + graph capture
 torch.cuda.synchronize()
 t0 = time.perf_counter()
