@@ -31,6 +31,7 @@ ranks on one GPU in the tests), ``LocalComm`` for one rank.
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -641,6 +642,70 @@ class DistGMG:
         return self._vc(top, b, out)
 
 
+class DistHierarchy:
+    """The slab decomposition of a GMG hierarchy, built once and re-linearised
+    every Newton iteration (the single-GPU path likewise keeps its Problems):
+    distributed levels (DistProblem), their transfers, the replicated coarse
+    Problems and the bridge between them."""
+
+    def __init__(self, global_meshes: list, degree: int, mat: Material, global_masks: list, comm,
+                 min_cells: int = 2, fine_dp: "DistProblem | None" = None):
+        nlev = len(global_meshes)
+        fine = global_meshes[-1]
+        self.comm, self.degree, self.nlev = comm, degree, nlev
+        self.slabs = level_slabs(fine.dim, degree, fine.cells, nlev, comm.rank, comm.size, min_cells)
+        first = next(i for i, s in enumerate(self.slabs) if s is not None)
+        if first == 0:
+            raise ValueError("the coarsest level must be replicated (min_cells too small for the hierarchy)")
+        self.first = first
+        self.dps = {i: (fine_dp if (i == nlev - 1 and fine_dp is not None) else
+                        DistProblem(global_meshes[i], degree, mat, self.slabs[i], comm, global_masks[i]))
+                    for i in range(first, nlev)}
+        self.transfers = [TransferOperator(self.dps[i].local, self.dps[i + 1].local) for i in range(first, nlev - 1)]
+        self.rep_probs = []
+        for i in range(first):
+            p = Problem(global_meshes[i], degree, mat)
+            p.constraints = ConstraintSet.from_dofs(p.n_dofs, np.flatnonzero(global_masks[i]))
+            self.rep_probs.append(p)
+        self.rep_transfers = build_transfers(self.rep_probs)
+        self.cslab = self.slabs[first].halved()
+        cs = self.cslab
+        self.coarse_local = Problem(sub_box(global_meshes[first - 1], cs.axis, cs.c0, cs.c1), degree, mat,
+                                    has_top_face=not cs.has_upper)
+        cmask = np.ascontiguousarray(cs.local(global_masks[first - 1]))
+        self.coarse_local.constraints = ConstraintSet.from_dofs(self.coarse_local.n_dofs, np.flatnonzero(cmask))
+        self.bridge = TransferOperator(self.coarse_local, self.dps[first].local)
+
+    @property
+    def fine(self) -> "DistProblem":
+        return self.dps[self.nlev - 1]
+
+    def build_gmg(self, u_fine_local, strategy: str = "tensor4", seed: int = 0, keep_constrained: bool = False):
+        """Linearise every level at the injected fine state (multigrid.py:358-382).
+        Returns (DistGMG, fine DistributedTangent)."""
+        first, nlev, dps = self.first, self.nlev, self.dps
+        u = {nlev - 1: dv.as_dev(u_fine_local)}
+        for lvl in range(nlev - 1, first, -1):  # injection down the slabs (multigrid.py:76-92)
+            uc = torch.empty(dps[lvl - 1].n_dofs, dtype=torch.float64, device="cuda")
+            check(lib().hf_inject(dps[lvl - 1].local._space, dps[lvl].local._space, dv.ptr(u[lvl]), dv.ptr(uc),
+                                  int(keep_constrained), dv.stream()))
+            u[lvl - 1] = uc
+        levels = [DistLevel(dps[i], u[i], strategy, seed + 7919 * i, i) for i in range(first, nlev)]
+        # full state on the finest replicated level: owned slices, all-reduced
+        cs = self.cslab
+        uc_local = torch.empty(cs.n_dofs, dtype=torch.float64, device="cuda")
+        check(lib().hf_inject(self.coarse_local._space, dps[first].local._space, dv.ptr(u[first]), dv.ptr(uc_local),
+                              int(keep_constrained), dv.stream()))
+        ufull = torch.zeros(cs.n_global_dofs, dtype=torch.float64, device="cuda")
+        o = cs.owned
+        ufull[cs.dof_offset + o.start:cs.dof_offset + o.stop] = uc_local[o]
+        self.comm.allreduce_(ufull)
+        rep_levels = build_level_operators(self.rep_probs, ufull, strategy, seed, keep_constrained)
+        replicated = GMGPreconditioner(rep_levels, self.rep_transfers)
+        gmg = DistGMG(levels, self.transfers, self.bridge, replicated, cs, self.comm)
+        return gmg, levels[-1].op
+
+
 def build_dist_gmg(global_meshes: list, degree: int, mat: Material, global_masks: list, u_fine_local, comm,
                    strategy: str = "tensor4", seed: int = 0, min_cells: int = 2, keep_constrained: bool = False,
                    fine_dp: "DistProblem | None" = None):
@@ -648,48 +713,48 @@ def build_dist_gmg(global_meshes: list, degree: int, mat: Material, global_masks
 
     ``global_meshes``/``global_masks``: every level, coarsest first.  Returns
     (DistGMG, fine DistProblem, fine DistributedTangent)."""
-    nlev = len(global_meshes)
-    fine = global_meshes[-1]
-    slabs = level_slabs(fine.dim, degree, fine.cells, nlev, comm.rank, comm.size, min_cells)
-    first = next(i for i, s in enumerate(slabs) if s is not None)
-    if first == 0:
-        raise ValueError("the coarsest level must be replicated (min_cells too small for the hierarchy)")
-    dps = {i: (fine_dp if (i == nlev - 1 and fine_dp is not None) else
-               DistProblem(global_meshes[i], degree, mat, slabs[i], comm, global_masks[i]))
-           for i in range(first, nlev)}
-    # injection of the fine state down the distributed levels (multigrid.py:76-92)
-    u = {nlev - 1: dv.as_dev(u_fine_local)}
-    for lvl in range(nlev - 1, first, -1):
-        uc = torch.empty(dps[lvl - 1].n_dofs, dtype=torch.float64, device="cuda")
-        check(lib().hf_inject(dps[lvl - 1].local._space, dps[lvl].local._space, dv.ptr(u[lvl]), dv.ptr(uc),
-                              int(keep_constrained), dv.stream()))
-        u[lvl - 1] = uc
-    levels = [DistLevel(dps[i], u[i], strategy, seed + 7919 * i, i) for i in range(first, nlev)]
-    transfers = [TransferOperator(dps[i].local, dps[i + 1].local) for i in range(first, nlev - 1)]
-    # replicated coarse levels: full coarse problems on every rank
-    rep_probs = []
-    for i in range(first):
-        p = Problem(global_meshes[i], degree, mat)
-        p.constraints = ConstraintSet.from_dofs(p.n_dofs, np.flatnonzero(global_masks[i]))
-        rep_probs.append(p)
-    # full state on the finest replicated level: owned slices, all-reduced
-    cslab = slabs[first].halved()
-    uc_local = torch.empty(cslab.n_dofs, dtype=torch.float64, device="cuda")
-    coarse_local = Problem(sub_box(global_meshes[first - 1], cslab.axis, cslab.c0, cslab.c1), degree, mat,
-                           has_top_face=not cslab.has_upper)
-    cmask = np.ascontiguousarray(cslab.local(global_masks[first - 1]))
-    coarse_local.constraints = ConstraintSet.from_dofs(coarse_local.n_dofs, np.flatnonzero(cmask))
-    check(lib().hf_inject(coarse_local._space, dps[first].local._space, dv.ptr(u[first]), dv.ptr(uc_local),
-                          int(keep_constrained), dv.stream()))
-    ufull = torch.zeros(cslab.n_global_dofs, dtype=torch.float64, device="cuda")
-    o = cslab.owned
-    ufull[cslab.dof_offset + o.start:cslab.dof_offset + o.stop] = uc_local[o]
-    comm.allreduce_(ufull)
-    rep_transfers = build_transfers(rep_probs)
-    rep_levels = build_level_operators(rep_probs, ufull, strategy, seed, keep_constrained)
-    replicated = GMGPreconditioner(rep_levels, rep_transfers)
-    bridge = TransferOperator(coarse_local, dps[first].local)
-    gmg = DistGMG(levels, transfers, bridge, replicated, cslab, comm)
-    gmg._keep = (coarse_local, rep_probs)
-    fine_op = levels[-1].op
-    return gmg, dps[nlev - 1], fine_op
+    h = DistHierarchy(global_meshes, degree, mat, global_masks, comm, min_cells, fine_dp)
+    gmg, op = h.build_gmg(u_fine_local, strategy, seed, keep_constrained)
+    gmg._hierarchy = h
+    return gmg, h.fine, op
+
+
+def newton_solve_prescribed_dist(h: DistHierarchy, settings, target: float, height_local: torch.Tensor,
+                                 strategy: str = "tensor4", seed: int = 0, on_record=None):
+    """Config-4 Newton (prescribed last-axis displacement) on the slab
+    decomposition: the restatement of solver.py:143-201 that
+    solver.newton_solve_prescribed runs on one GPU, with all-reduced norms.
+    ``height_local``: X_last / max X_last on this rank's DoF slice (node-blocked)."""
+    from .solver import MaxNewtonIterations, NewtonRecord
+
+    dp = h.fine
+    d = dp.local.dim
+    u = torch.zeros(dp.n_dofs, dtype=torch.float64, device="cuda")
+    s = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def norm(v):
+        return float(np.sqrt(dp.dot(v, v, s).item()))
+
+    records = []
+    for step in range(1, settings.n_load_steps + 1):
+        u.view(-1, d)[:, d - 1] += (target / settings.n_load_steps) * height_local
+        residual = dp.residual(u)
+        res0 = norm(residual)
+        res_target = max(settings.residual_rel_tol * res0, settings.residual_abs_tol)
+        for it in range(1, settings.max_newton_iterations + 1):
+            gmg, op = h.build_gmg(u, strategy, seed, keep_constrained=True)
+            t0 = time.perf_counter()
+            du, its, _, _ = dist_cg(dp, op, -residual, rel_tol=settings.linear_rel_tol, preconditioner=gmg)
+            t_cg = time.perf_counter() - t0
+            u += du
+            residual = dp.residual(u)
+            res_norm, du_norm = norm(residual), norm(du)
+            rec = NewtonRecord(step, step / settings.n_load_steps, it, res_norm, du_norm, its, t_cg)
+            records.append(rec)
+            if on_record:
+                on_record(rec)
+            if du_norm <= settings.update_tol and res_norm <= res_target:
+                break
+        else:
+            raise MaxNewtonIterations("no convergence in the distributed prescribed-displacement Newton", records)
+    return u, records

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--backend", default="gloo")
     ap.add_argument("--cells", type=int, default=16)
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--newton", action="store_true", help="config-4 prescribed-displacement Newton instead")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = local % max(torch.cuda.device_count(), 1)
@@ -41,6 +42,8 @@ def main():
     from paper_1904_13131_b200.workloads import AMP_SOLVE, MATERIAL, host_workload
 
     comm = TorchComm()
+    if args.newton:
+        return newton_main(args, comm)
     wl = host_workload(args.config, seed=0, amp=AMP_SOLVE, levels=True, m=args.cells)
     p = wl.cfg["degree"]
     probs = []
@@ -91,6 +94,43 @@ def main():
     out = dict(zip(keys, worst[:-1].tolist()))
     out.update(cg_iterations_single=rep.iterations, cg_iterations_dist=int(worst[-1].item()), size=comm.size,
                backend=args.backend, n_global_dofs=res["n_global_dofs"], levels=[m.cells[-1] for m in wl.meshes])
+    if comm.rank == 0:
+        print("DISTRESULT " + json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
+def newton_main(args, comm):
+    """Single-GPU newton_solve_prescribed vs newton_solve_prescribed_dist (config 4 recipe)."""
+    from paper_1904_13131_b200 import NewtonSettings, newton_solve_prescribed
+    from paper_1904_13131_b200.distributed import DistHierarchy, newton_solve_prescribed_dist
+    from paper_1904_13131_b200.fespace import ConstraintSet, build_dof_map, node_coordinates
+    from paper_1904_13131_b200.operators import Problem
+    from paper_1904_13131_b200.workloads import MATERIAL, host_workload
+
+    wl = host_workload(4, seed=0, levels=True, m=args.cells, with_x=False)
+    probs = []
+    for mesh, mask in zip(wl.meshes, wl.masks):
+        pr = Problem(mesh, 2, MATERIAL)
+        pr.constraints = ConstraintSet.from_dofs(pr.n_dofs, np.flatnonzero(mask))
+        probs.append(pr)
+    settings = NewtonSettings(n_load_steps=2)
+    single = newton_solve_prescribed(probs, settings, -0.05)
+    h = DistHierarchy(wl.meshes, 2, MATERIAL, wl.masks, comm)
+    fine = wl.meshes[-1]
+    X = node_coordinates(fine, build_dof_map(fine, 2, 3))
+    hgt = X[:, 2] / X[:, 2].max()
+    sl = h.fine.slab
+    hl = torch.from_numpy(np.ascontiguousarray(hgt[sl.dof_offset // 3:(sl.dof_offset + sl.n_dofs) // 3])).cuda()
+    u, recs = newton_solve_prescribed_dist(h, settings, -0.05, hl)
+    a = np.array([(r.load_step, r.iteration, r.residual_norm, r.cg_iterations) for r in single.records])
+    b = np.array([(r.load_step, r.iteration, r.residual_norm, r.cg_iterations) for r in recs])
+    ul = sl.local(single.u)
+    out = dict(size=comm.size, newton=True, single=a.tolist(), dist=b.tolist(),
+               u_rel=float(torch.linalg.norm(u - ul) / torch.linalg.norm(ul)))
+    t = torch.tensor([out["u_rel"]], dtype=torch.float64)
+    if comm.size > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    out["u_rel"] = t.item()
     if comm.rank == 0:
         print("DISTRESULT " + json.dumps(out), flush=True)
     dist.destroy_process_group()

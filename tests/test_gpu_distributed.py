@@ -21,10 +21,10 @@ def _port():
         return s.getsockname()[1]
 
 
-def _run(nproc, m, backend="gloo", cfg=2):
+def _run(nproc, m, backend="gloo", cfg=2, extra=()):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", "dist_worker.py"),
-           "--backend", backend, "--cells", str(m), "--config", str(cfg)]
+           "--backend", backend, "--cells", str(m), "--config", str(cfg), *extra]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in p.stdout.splitlines() if l.startswith("DISTRESULT ")]
     assert p.returncode == 0 and lines, p.stdout[-3000:] + p.stderr[-3000:]
@@ -40,3 +40,20 @@ def test_slab_decomposition_matches_single_gpu(nproc, m):
         assert r[k] < 1e-12, (k, r[k])
     assert abs(r["cg_iterations_dist"] - r["cg_iterations_single"]) <= 1, r
     assert r["cg_solution"] < 1e-6, r
+
+
+@pytest.mark.gpu
+def test_prescribed_newton_on_slabs_matches_single_gpu():
+    """Config-4 Newton (SURVEY H5 restatement) on 2 slabs vs one GPU: same
+    Newton iterations, CG counts +-1, residual histories, solution."""
+    import numpy as np
+
+    r = _run(2, 8, extra=("--newton",))
+    a, b = np.array(r["single"]), np.array(r["dist"])
+    assert a.shape == b.shape
+    assert np.array_equal(a[:, :2], b[:, :2])
+    assert np.all(np.abs(a[:, 3] - b[:, 3]) <= 1)
+    assert np.allclose(a[:, 2], b[:, 2], rtol=1e-3, atol=1e-11)
+    # each Newton step's CG stops at rel 1e-6 (solver.py:85): the two paths' final
+    # states agree to the Newton tolerance, not to rounding
+    assert r["u_rel"] < 1e-6
