@@ -18,8 +18,13 @@
  *    hot-path calls are asynchronous on that stream, setup calls synchronise;
  *  - vectors use the reference layout: lexicographic lattice nodes (x
  *    fastest), DoF = node * dim + component (fespace.py:3-8);
- *  - per-q-point arrays are SoA: field f of q-point (cell e, local q) at
- *    f * n_qp + e * nq + q.
+ *  - the geometry arrays (hf_space_pointers / hf_space_geometry_copy) are SoA:
+ *    field f of q-point (cell e, local q) at f * n_qp + e * nq + q; the
+ *    tangents' q-point caches are internal (tiled per warp);
+ *  - a tangent created with storage_bits = 32 (hf_tangent_create_ex) takes
+ *    float x / y arrays in every apply entry point; all others take double;
+ *  - handles are not thread-safe; the reduction workspace (hf_ws) must not be
+ *    shared by concurrently running streams.
  */
 #ifndef HF_H
 #define HF_H
