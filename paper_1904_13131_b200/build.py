@@ -17,12 +17,13 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build_obj")
-LIB = os.path.join(PKG, "libhf.so")
+DEBUG = os.environ.get("HF_DEBUG", "0") not in ("", "0")  # device bounds checks -> libhf_debug.so
+OBJ = os.path.join(PKG, "build_obj_debug" if DEBUG else "build_obj")
+LIB = os.path.join(PKG, "libhf_debug.so" if DEBUG else "libhf.so")
 SOURCES = ["hf_api.cu", "hf_cells2d.cu", "hf_cells3d.cu", "hf_assemble.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-         "-I", os.path.join(ROOT, "include")]
+         "-I", os.path.join(ROOT, "include")] + (["-DHF_DEBUG"] if DEBUG else [])
 
 
 def _nvcc() -> str:

@@ -88,6 +88,7 @@ struct hf_tangent {
   hf_space* sp;
   int strategy;
   int nf;
+  long long cache_len = 0;  // elements
   int fp32 = 0;  // cache and x/y stored as float (mixed-precision multigrid levels)
   double* d_cache = nullptr;
   double* d_ubar = nullptr;
@@ -408,6 +409,7 @@ HF_API int hf_tangent_create_ex(hf_space* sp, int strategy, int storage_bits, co
   op->fp32 = storage_bits == 32;
   const int esz = op->fp32 ? 4 : 8;
   const long long ncache = tile_cache_doubles(sp->dim, sp->n1, op->nf, sp->lat.n_el, esz);
+  op->cache_len = ncache;
   HF_CUDA(cudaMalloc((void**)&op->d_cache, (size_t)esz * (ncache > 0 ? ncache : 1)));
   if (strategy == HF_SCALAR) {
     HF_CUDA(cudaMalloc((void**)&op->d_ubar, sizeof(double) * sp->n_dofs));
@@ -420,6 +422,7 @@ HF_API int hf_tangent_create_ex(hf_space* sp, int strategy, int storage_bits, co
   a.cache_out = op->d_cache;
   a.detmin = sp->d_u64;
   a.fp32 = op->fp32;
+  a.cache_len = op->cache_len;
   HF_CUDA(cell(sp, OP_BUILD, strategy, a, s));
   unsigned long long o;
   HF_CUDA(cudaMemcpyAsync(&o, sp->d_u64, sizeof(o), cudaMemcpyDeviceToHost, s));
@@ -444,6 +447,7 @@ static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, con
   a.tile0 = tile0;
   a.tile1 = tile1;
   a.fp32 = op->fp32;
+  a.cache_len = op->cache_len;
   a.x = x_dev;
   a.y = y_dev;
   a.cache = op->d_cache;

@@ -67,6 +67,7 @@ struct CellArgs {
   const int* skip;          // optional device flag; non-zero -> kernel is a no-op
   int fill;                 // apply: 0 plain, 1/2 PDL secondary (hf_line.cuh LineArgs::fill)
   int fp32;                 // apply/build: cache and x/y stored as float (mixed-precision levels)
+  long long cache_len;      // cache elements (bounds checks of the debug build)
   long long tile0, tile1;   // apply: tile range; tile1 < 0 means all tiles
   unsigned long long* detmin;  // ordered-double min of det F (build / residual / range)
   unsigned long long* detmax;
@@ -439,7 +440,11 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_build(const CellArgs a) {
   constexpr int NF = CacheFields<DIM, VAR>::NF;
   using TL = TileLayout<DIM, N>;
   ST* o = reinterpret_cast<ST*>(a.cache_out);  // fp64, or fp32 storage of a mixed-precision level
-  auto put = [&](int f, double v) { o[TL::template index_e<sizeof(ST)>(t.e, t.lq, f, NF)] = (ST)v; };
+  auto put = [&](int f, double v) {
+    const long long i = TL::template index_e<sizeof(ST)>(t.e, t.lq, f, NF);
+    HF_ASSERT(i >= 0 && i < a.cache_len);
+    o[i] = (ST)v;
+  };
   int f = 0;
   if (VAR == SCALAR) {
     put(f++, k.c1);

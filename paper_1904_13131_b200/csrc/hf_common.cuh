@@ -5,6 +5,24 @@
 
 #define HF_DEV __device__ __forceinline__
 
+// Device-side bounds checks of the debug build (HF_DEBUG=1 python -m
+// paper_1904_13131_b200.build -> libhf_debug.so): compute-sanitizer is not
+// available on the GPU pool, so index arithmetic is checked by the kernels.
+#ifdef HF_DEBUG
+#include <cstdio>
+#define HF_ASSERT(c)                                                                  \
+  do {                                                                                \
+    if (!(c)) {                                                                       \
+      printf("HF_ASSERT %s:%d: %s\n", __FILE__, __LINE__, #c);                        \
+      __trap();                                                                       \
+    }                                                                                 \
+  } while (0)
+#else
+#define HF_ASSERT(c) \
+  do {               \
+  } while (0)
+#endif
+
 // Largest 1D table the cell kernels are instantiated for (2D p<=8).
 #define HF_MAXN 9
 

@@ -69,6 +69,7 @@ struct LineArgs {
   // 2: PDL secondary of a kernel that wrote x and y (hf_cheb_step_fill): wait before the first gather
   int fill;
   long long tile0, tile1;  // tile range of this launch (interior/boundary split of a slab)
+  long long cache_len;     // cache elements (bounds checks of the debug build)
 };
 
 // Per-warp line-buffer layout: element (cell m, component c, point i,j,k) at
@@ -192,6 +193,7 @@ HF_DEV void gather_tile(const LineArgs& a, long long tile, long long ntiles, int
 #pragma unroll
   for (int l = 0; l < N; ++l) {
     const long long d0 = (nb + l * s_last) * DIM;
+    HF_ASSERT(d0 >= 0 && d0 + DIM <= a.lat.n_nodes * DIM);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
       g.u[c][l] = (double)__ldg(xs + d0 + c);
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     const long long tile = a.tile0 + blockIdx.x + (warp + (j / N) * W) * (long long)gridDim.x;
     if (tile >= ntiles) return;
     const int s = (int)(j % RW);
+    HF_ASSERT(tile * tstride + (j % N + 1) * CH <= a.cache_len);
     mbar_expect_tx(full + s, (unsigned)(CH * sizeof(ST)));
     tma_load_1d(ring + (size_t)s * CH, cache + tile * tstride + (j % N) * CH, (unsigned)(CH * sizeof(ST)), full + s);
   };
@@ -571,6 +574,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 #pragma unroll
       for (int l = 0; l < N; ++l) {
         const long long d0 = (nb + l * s_last) * DIM;
+        HF_ASSERT(d0 >= 0 && d0 + DIM <= a.lat.n_nodes * DIM);
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc)
           if (!((g.mb >> (cc * N + l)) & 1u)) atomicAdd(reinterpret_cast<ST*>(a.y) + d0 + cc, (ST)v[cc][l]);
