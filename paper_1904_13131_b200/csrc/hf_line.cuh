@@ -41,6 +41,7 @@
 // fespace.py:258-288; scatter fespace.py:296-324.
 #pragma once
 #include "hf_cell.cuh"
+#include "hf_lanemap_q2.h"
 
 namespace hf {
 
@@ -115,23 +116,71 @@ HF_DEV void c1d(const double (&M)[N][N], const double* in, double* out) {
   }
 }
 
-template <int DIM, int N, int AX>
-HF_DEV void ld_line(const double* cell, int t, double (&v)[DIM][N]) {
+// Where a thread's line sites live in its warp's line buffers: off[AX][l] is
+// the offset (component 0) of the site at position l along axis AX of the
+// line the thread owns in an AX phase.  3D Q2 uses the generated
+// bank-conflict-free map (hf_lanemap_q2.h: lane -> (cell, line) slot, sites
+// coloured over the 16 banks of each half-warp); other (DIM, N) the padded
+// interleaved layout of LineLay.
+template <int DIM, int N>
+struct LineMap {
+  static constexpr bool CUSTOM = DIM == 3 && N == 3;
+  static constexpr int CS = CUSTOM ? kQ2Comp : LineLay<DIM, N>::NP * LineLay<DIM, N>::CPWP;  // component stride
+  static constexpr int BUF = DIM * CS;                                                      // doubles per buffer
+};
+
+template <int DIM, int N>
+struct LineOff {
+  int off[DIM][N];
+};
+
+// lane -> (slot = cell * L + line, cell m, line t, active) and its site offsets
+template <int DIM, int N>
+HF_DEV void line_map(int lane, int& slot, int& m, int& t, bool& act, LineOff<DIM, N>& o) {
+  using K = LineCfg<DIM, N>;
   using Y = LineLay<DIM, N>;
-  const int b = lbase<DIM, N, AX>(t);
+  if constexpr (LineMap<DIM, N>::CUSTOM) {
+    const unsigned long long w = lane < 12 ? kQ2SlotBits0 : (lane < 24 ? kQ2SlotBits1 : kQ2SlotBits2);
+    const int sl = (int)((w >> (5 * (lane % 12))) & 31ull);
+    act = sl != 31;
+    slot = act ? sl : 0;
+    m = slot / K::L;
+    t = slot - m * K::L;
+    int q[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    q2_offsets(slot, q);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int l = 0; l < N; ++l) o.off[a][l] = q[a < 3 ? a : 0][l < 3 ? l : 0];
+  } else {
+    act = lane < K::LANES;
+    m = act ? lane / K::L : 0;
+    t = act ? lane - m * K::L : 0;
+    slot = m * K::L + t;
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      o.off[0][l] = (lbase<DIM, N, 0>(t) + l * lstride<DIM, N, 0>()) * Y::CPWP + m;
+      o.off[1][l] = (lbase<DIM, N, 1>(t) + l * lstride<DIM, N, 1>()) * Y::CPWP + m;
+      if (DIM == 3) o.off[DIM - 1][l] = (lbase<DIM, N, DIM - 1>(t) + l * lstride<DIM, N, DIM - 1>()) * Y::CPWP + m;
+    }
+  }
+}
+
+template <int DIM, int N, int AX>
+HF_DEV void ld_line(const double* buf, const LineOff<DIM, N>& o, double (&v)[DIM][N]) {
+  constexpr int CS = LineMap<DIM, N>::CS;
 #pragma unroll
   for (int c = 0; c < DIM; ++c)
 #pragma unroll
-    for (int l = 0; l < N; ++l) v[c][l] = cell[(c * Y::NP + b + l * lstride<DIM, N, AX>()) * Y::CPWP];
+    for (int l = 0; l < N; ++l) v[c][l] = buf[c * CS + o.off[AX][l]];
 }
 template <int DIM, int N, int AX>
-HF_DEV void st_line(double* cell, int t, const double (&v)[DIM][N]) {
-  using Y = LineLay<DIM, N>;
-  const int b = lbase<DIM, N, AX>(t);
+HF_DEV void st_line(double* buf, const LineOff<DIM, N>& o, const double (&v)[DIM][N]) {
+  constexpr int CS = LineMap<DIM, N>::CS;
 #pragma unroll
   for (int c = 0; c < DIM; ++c)
 #pragma unroll
-    for (int l = 0; l < N; ++l) cell[(c * Y::NP + b + l * lstride<DIM, N, AX>()) * Y::CPWP] = v[c][l];
+    for (int l = 0; l < N; ++l) buf[c * CS + o.off[AX][l]] = v[c][l];
 }
 template <int DIM, int N, bool TR>
 HF_DEV void c_line(const double (&M)[N][N], double (&v)[DIM][N]) {
@@ -208,8 +257,8 @@ HF_DEV void gather_tile(const LineArgs& a, long long tile, long long ntiles, int
 // (x-line owners), the axis-1 derivative in buffer g1, axis-2 (3D) in g2.
 // Buffers a and b are scratch.
 template <int DIM, int N>
-HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live, int t, double* a, double* b,
-                      double* g1, double* g2, double (&Gx)[DIM][N]) {
+HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live, const LineOff<DIM, N>& t,
+                      double* a, double* b, double* g1, double* g2, double (&Gx)[DIM][N]) {
   double u[DIM][N];
   if (live) {
 #pragma unroll
@@ -298,7 +347,7 @@ struct LinePlan {
   static constexpr long long CH = TileLayout<DIM, N>::template chunk_e<sizeof(ST)>(NF);
   static constexpr size_t BUDGET = 226 * 1024;
   static constexpr size_t perw(int rw) {
-    return sizeof(ST) * (size_t)rw * CH + sizeof(double) * (size_t)NB * LineLay<DIM, N>::BUF + 16 * rw;
+    return sizeof(ST) * (size_t)rw * CH + sizeof(double) * (size_t)NB * LineMap<DIM, N>::BUF + 16 * rw;
   }
   // RW = min(N, 3) stages: at Q2 the chunks of the next tile are issued while
   // the current tile's point phase consumes its own, one tile period ahead of
@@ -319,7 +368,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     k_apply_line(const LineArgs a, const TabLine<N> T) {
   using K = LineCfg<DIM, N>;
   using PL = LinePlan<DIM, N, VAR, ST>;
-  using Y = LineLay<DIM, N>;
+  using Y = LineMap<DIM, N>;
   constexpr int NF = PL::NF;
   constexpr int NB = PL::NB;
   constexpr int W = PL::W;
@@ -358,10 +407,11 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   bool synced = a.fill != 1;
   if (a.fill == 2) asm volatile("griddepcontrol.wait;" ::: "memory");  // x comes from the primary
 
-  const int m = lane / K::L;
-  const int t = lane - m * K::L;
-  const bool act = lane < K::LANES;
-  double* wb = lbuf + (size_t)warp * NB * Y::BUF + (act ? m : 0);
+  int slot, m, t;
+  bool act;
+  LineOff<DIM, N> lo;
+  line_map<DIM, N>(lane, slot, m, t, act, lo);
+  double* wb = lbuf + (size_t)warp * NB * Y::BUF;
   double* bufs[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) bufs[b] = wb + b * Y::BUF;
@@ -387,8 +437,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 
     double Gx[DIM][N];
     double Gxu[DIM][N];  // scalar: x part of the gradient of ubar
-    if (VAR == SCALAR) eval_line<DIM, N>(T, g.ub, live, t, Q, Sc, bufs[3], bufs[4], Gxu);
-    eval_line<DIM, N>(T, u, live, t, Q, Sc, G1, G2, Gx);
+    if (VAR == SCALAR) eval_line<DIM, N>(T, g.ub, live, lo, Q, Sc, bufs[3], bufs[4], Gxu);
+    eval_line<DIM, N>(T, u, live, lo, Q, Sc, G1, G2, Gx);
 
     // ---------------- P: q-point physics along this thread's x-line ----------------
     double mu = 0.0, lam = 0.0;
@@ -396,11 +446,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       mu = __ldg(a.mu + e);
       lam = __ldg(a.lam + e);
     }
-    const int pt0 = lbase<DIM, N, 0>(t);
     // one Gauss point of this thread's x-line from its cache chunk
     auto point = [&](const int iq, const ST* st) {
       if (live) {
-      const int pt = pt0 + iq;
+      const int pt = lo.off[0][iq];  // this thread's x-line site iq
       double f[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q) f[q] = (double)st[q * K::LANES];
@@ -408,8 +457,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 #pragma unroll
       for (int cc = 0; cc < DIM; ++cc) {
         gu[cc][0] = Gx[cc][iq];
-        gu[cc][1] = G1[(cc * Y::NP + pt) * Y::CPWP];
-        if (DIM == 3) gu[cc][DIM - 1] = G2[(cc * Y::NP + pt) * Y::CPWP];
+        gu[cc][1] = G1[cc * Y::CS + pt];
+        if (DIM == 3) gu[cc][DIM - 1] = G2[cc * Y::CS + pt];
       }
       double G[DIM][DIM];
       if (VAR == TENSOR4) {
@@ -443,8 +492,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc) {
           gub[cc][0] = Gxu[cc][iq];
-          gub[cc][1] = bufs[3][(cc * Y::NP + pt) * Y::CPWP];
-          if (DIM == 3) gub[cc][DIM - 1] = bufs[4][(cc * Y::NP + pt) * Y::CPWP];
+          gub[cc][1] = bufs[3][cc * Y::CS + pt];
+          if (DIM == 3) gub[cc][DIM - 1] = bufs[4][cc * Y::CS + pt];
         }
         double F[DIM * DIM];
 #pragma unroll
@@ -481,9 +530,9 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       }
 #pragma unroll
       for (int cc = 0; cc < DIM; ++cc) {
-        Q[(cc * Y::NP + pt) * Y::CPWP] = G[cc][0];
-        G1[(cc * Y::NP + pt) * Y::CPWP] = G[cc][1];
-        if (DIM == 3) G2[(cc * Y::NP + pt) * Y::CPWP] = G[cc][DIM - 1];
+        Q[cc * Y::CS + pt] = G[cc][0];
+        G1[cc * Y::CS + pt] = G[cc][1];
+        if (DIM == 3) G2[cc * Y::CS + pt] = G[cc][DIM - 1];
       }
     }
     };
@@ -493,7 +542,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 #pragma unroll
       for (int iq = 0; iq < N; ++iq) mbar_wait(full + (int)((jc + iq) % RW), (unsigned)(((jc + iq) / RW) & 1));
 #pragma unroll
-      for (int iq = 0; iq < N; ++iq) point(iq, ring + (size_t)((jc + iq) % RW) * CH + lane);
+      for (int iq = 0; iq < N; ++iq) point(iq, ring + (size_t)((jc + iq) % RW) * CH + slot);
       __syncwarp();
       if (lane == 0) {  // stages consumed by every lane: refill them with the next tile's chunks
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -506,7 +555,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       for (int iq = 0; iq < N; ++iq, ++jc) {
         const int s = (int)(jc % RW);
         mbar_wait(full + s, (unsigned)((jc / RW) & 1));
-        point(iq, ring + (size_t)s * CH + lane);
+        point(iq, ring + (size_t)s * CH + slot);
         __syncwarp();
         if (lane == 0) {  // stage consumed by every lane: refill it with chunk jc + RW
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -518,45 +567,45 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     // ---------------- I1: transposed collocation derivative per axis, in place ----------------
     if (live) {
       double v[DIM][N];
-      ld_line<DIM, N, 0>(Q, t, v);
+      ld_line<DIM, N, 0>(Q, lo, v);
       c_line<DIM, N, true>(T.Dc, v);
-      st_line<DIM, N, 0>(Q, t, v);
-      ld_line<DIM, N, 1>(G1, t, v);
+      st_line<DIM, N, 0>(Q, lo, v);
+      ld_line<DIM, N, 1>(G1, lo, v);
       c_line<DIM, N, true>(T.Dc, v);
-      st_line<DIM, N, 1>(G1, t, v);
+      st_line<DIM, N, 1>(G1, lo, v);
       if (DIM == 3) {
-        ld_line<DIM, N, DIM - 1>(G2, t, v);
+        ld_line<DIM, N, DIM - 1>(G2, lo, v);
         c_line<DIM, N, true>(T.Dc, v);
-        st_line<DIM, N, DIM - 1>(G2, t, v);
+        st_line<DIM, N, DIM - 1>(G2, lo, v);
       }
     }
     __syncwarp();
     // ---------------- I2: sum, transposed interpolation along x ----------------
     if (live) {
       double v[DIM][N], w[DIM][N];
-      ld_line<DIM, N, 0>(Q, t, v);
-      ld_line<DIM, N, 0>(G1, t, w);
+      ld_line<DIM, N, 0>(Q, lo, v);
+      ld_line<DIM, N, 0>(G1, lo, w);
 #pragma unroll
       for (int cc = 0; cc < DIM; ++cc)
 #pragma unroll
         for (int l = 0; l < N; ++l) v[cc][l] += w[cc][l];
       if (DIM == 3) {
-        ld_line<DIM, N, 0>(G2, t, w);
+        ld_line<DIM, N, 0>(G2, lo, w);
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc)
 #pragma unroll
           for (int l = 0; l < N; ++l) v[cc][l] += w[cc][l];
       }
       c_line<DIM, N, true>(T.V, v);
-      st_line<DIM, N, 0>(Q, t, v);
+      st_line<DIM, N, 0>(Q, lo, v);
     }
     __syncwarp();
     if (DIM == 3) {
       if (live) {
         double v[DIM][N];
-        ld_line<DIM, N, 1>(Q, t, v);
+        ld_line<DIM, N, 1>(Q, lo, v);
         c_line<DIM, N, true>(T.V, v);
-        st_line<DIM, N, 1>(Q, t, v);
+        st_line<DIM, N, 1>(Q, lo, v);
       }
       __syncwarp();
     }
@@ -567,7 +616,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     }
     if (live) {
       double v[DIM][N];
-      ld_line<DIM, N, DIM - 1>(Q, t, v);
+      ld_line<DIM, N, DIM - 1>(Q, lo, v);
       c_line<DIM, N, true>(T.V, v);
       long long nb, s_last;
       last_axis_line<DIM, N>(a.lat, g.node0, t, nb, s_last);
