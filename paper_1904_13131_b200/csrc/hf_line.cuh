@@ -544,10 +544,9 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 #pragma unroll
       for (int iq = 0; iq < N; ++iq) point(iq, ring + (size_t)((jc + iq) % RW) * CH + slot);
       __syncwarp();
-      if (lane == 0) {  // stages consumed by every lane: refill them with the next tile's chunks
+      if (lane < N) {  // stages consumed by every lane: lanes 0..N-1 refill them with the next tile's chunks
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#pragma unroll 1
-        for (int iq = 0; iq < N; ++iq) issue(jc + iq + RW);
+        issue(jc + lane + RW);
       }
       jc += N;
     } else {
