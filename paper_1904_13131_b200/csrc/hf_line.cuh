@@ -41,7 +41,7 @@
 // fespace.py:258-288; scatter fespace.py:296-324.
 #pragma once
 #include "hf_cell.cuh"
-#include "hf_lanemap_q2.h"
+#include "hf_lanemap.h"
 
 namespace hf {
 
@@ -119,13 +119,13 @@ HF_DEV void c1d(const double (&M)[N][N], const double* in, double* out) {
 // Where a thread's line sites live in its warp's line buffers: off[AX][l] is
 // the offset (component 0) of the site at position l along axis AX of the
 // line the thread owns in an AX phase.  3D Q2 uses the generated
-// bank-conflict-free map (hf_lanemap_q2.h: lane -> (cell, line) slot, sites
+// bank-conflict-free map (hf_lanemap.h: lane -> (cell, line) slot, sites
 // coloured over the 16 banks of each half-warp); other (DIM, N) the padded
 // interleaved layout of LineLay.
 template <int DIM, int N>
 struct LineMap {
-  static constexpr bool CUSTOM = DIM == 3 && N == 3;
-  static constexpr int CS = CUSTOM ? kQ2Comp : LineLay<DIM, N>::NP * LineLay<DIM, N>::CPWP;  // component stride
+  static constexpr bool CUSTOM = LaneMapT<DIM, N>::ENABLED;
+  static constexpr int CS = CUSTOM ? LaneMapT<DIM, N>::COMP : LineLay<DIM, N>::NP * LineLay<DIM, N>::CPWP;  // component stride
   static constexpr int BUF = DIM * CS;                                                      // doubles per buffer
 };
 
@@ -140,18 +140,19 @@ HF_DEV void line_map(int lane, int& slot, int& m, int& t, bool& act, LineOff<DIM
   using K = LineCfg<DIM, N>;
   using Y = LineLay<DIM, N>;
   if constexpr (LineMap<DIM, N>::CUSTOM) {
-    const unsigned long long w = lane < 12 ? kQ2SlotBits0 : (lane < 24 ? kQ2SlotBits1 : kQ2SlotBits2);
+    using Z = LaneMapT<DIM, N>;
+    const unsigned long long w = lane < 12 ? Z::B0 : (lane < 24 ? Z::B1 : Z::B2);
     const int sl = (int)((w >> (5 * (lane % 12))) & 31ull);
     act = sl != 31;
     slot = act ? sl : 0;
     m = slot / K::L;
     t = slot - m * K::L;
-    int q[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    q2_offsets(slot, q);
+    int q[3][N] = {};
+    Z::offsets(slot, q);
 #pragma unroll
     for (int a = 0; a < DIM; ++a)
 #pragma unroll
-      for (int l = 0; l < N; ++l) o.off[a][l] = q[a < 3 ? a : 0][l < 3 ? l : 0];
+      for (int l = 0; l < N; ++l) o.off[a][l] = q[a < 3 ? a : 0][l];
   } else {
     act = lane < K::LANES;
     m = act ? lane / K::L : 0;
