@@ -124,6 +124,21 @@ HF_API int hf_tangent_apply_after_fill(hf_tangent* op, const double* x_dev, doub
 HF_API int hf_tangent_tiles(const hf_tangent* op, long long* n_tiles, int* cells_per_tile);
 HF_API int hf_tangent_apply_tiles(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
                                   long long tile0, long long tile1, int mode, void* stream);
+/* Host-to-host .apply for callers that hold the vectors in host memory (the
+ * reference's numpy arrays, operators.py:331-339): y_host = A x_host.  Both
+ * buffers must be page-locked (cudaHostAlloc / pinned torch tensors, or
+ * registered with hf_host_register).  The cells are cut into `chunks` slabs of
+ * last-axis cell layers; the H2D copy of a slab's node planes, its fill + cell
+ * kernel, and the D2H copy of finished planes run on three streams, so the
+ * copies overlap each other and the kernels.  The pipeline is captured as a
+ * CUDA graph on first use per (x_host, y_host, chunks) and replayed after
+ * that (a few cached per tangent).  Asynchronous on `stream`: y_host is ready
+ * once the stream is synchronised.  Uses device staging vectors owned by the
+ * tangent, so calls on one tangent must not run concurrently. */
+HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y_host, int chunks, void* stream);
+/* page-lock / release caller-owned host memory (cudaHostRegister) */
+HF_API int hf_host_register(void* host_ptr, long long bytes);
+HF_API int hf_host_unregister(void* host_ptr);
 /* matrix-based baseline (assemble_matrix / AssembledTangent, operators.py:436-516):
  * vals_dev (n_el, nld, nld) element matrices of a tensor4 tangent, nld = nloc*dim,
  * local DoF n*dim + c; dofs_dev (n_el, nld) their global DoFs (operators.py:474).

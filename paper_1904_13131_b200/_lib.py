@@ -51,6 +51,9 @@ _SIGS = {
     "hf_tangent_apply_after_fill": (I, [P, P, P, P, P]),
     "hf_tangent_tiles": (I, [P, ct.POINTER(LL), ct.POINTER(I)]),
     "hf_tangent_apply_tiles": (I, [P, P, P, P, LL, LL, I, P]),
+    "hf_tangent_apply_host": (I, [P, P, P, I, P]),
+    "hf_host_register": (I, [P, LL]),
+    "hf_host_unregister": (I, [P]),
     "hf_tangent_diagonal": (I, [P, P, P]),
     "hf_tangent_assemble_local": (I, [P, P, P]),
     "hf_space_cell_dofs": (I, [P, P, P]),

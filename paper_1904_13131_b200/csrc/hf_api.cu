@@ -2,6 +2,7 @@
 // contract and the reference interface each entry point replaces.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -84,6 +85,26 @@ struct hf_space {
   unsigned long long* d_u64 = nullptr;  // [0] detmin [1] detmax [2] first-index
 };
 
+// Host-to-host apply (hf_tangent_apply_host): device staging vectors, copy
+// streams, and the pipelines already captured as CUDA graphs, keyed by the
+// host buffers and the slab count.
+struct HostPipe {
+  static constexpr int NG = 4;
+  double* xd = nullptr;
+  double* yd = nullptr;
+  cudaStream_t cap = nullptr, s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev;
+  struct Entry {
+    const void* x;
+    void* y;
+    int chunks;
+    cudaGraphExec_t exec;
+    unsigned long long used;
+  } g[NG] = {};
+  int ng = 0;
+  unsigned long long clock = 0;
+};
+
 struct hf_tangent {
   hf_space* sp;
   int strategy;
@@ -92,6 +113,7 @@ struct hf_tangent {
   int fp32 = 0;  // cache and x/y stored as float (mixed-precision multigrid levels)
   double* d_cache = nullptr;
   double* d_ubar = nullptr;
+  HostPipe* host = nullptr;
 };
 
 struct hf_transfer {
@@ -513,6 +535,183 @@ HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, 
   return hf_tangent_apply_flagged(op, x_dev, y_dev, nullptr, stream);
 }
 
+// ---- host-to-host apply: slab pipeline captured once per buffer pair ----
+static void host_pipe_free(HostPipe* h) {
+  if (!h) return;
+  for (int i = 0; i < h->ng; ++i) cudaGraphExecDestroy(h->g[i].exec);
+  for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  if (h->cap) cudaStreamDestroy(h->cap);
+  if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_out) cudaStreamDestroy(h->s_out);
+  cudaFree(h->xd);
+  cudaFree(h->yd);
+  delete h;
+}
+
+static bool page_locked(const void* p, long long bytes) {
+  const char* c = static_cast<const char*>(p);
+  for (const char* q : {c, c + (bytes > 0 ? bytes - 1 : 0)}) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.type != cudaMemoryTypeHost) return false;
+  }
+  return true;
+}
+
+// Enqueue y_host = A x_host on h->cap (being captured).  The cells are cut
+// into `chunks` slabs of last-axis cell layers; cells are lexicographic with
+// the last axis slowest, so a slab touches a contiguous range of node planes,
+// i.e. a contiguous DoF range.  H2D of each slab's new planes runs on s_in,
+// fill + cell kernel on cap, D2H of the planes no later slab touches on s_out.
+static int host_pipe_enqueue(hf_tangent* op, HostPipe* h, const double* xh, double* yh, int chunks) {
+  const hf_space* sp = op->sp;
+  const int d = sp->dim, deg = sp->degree;
+  const long long layer = d == 3 ? (long long)sp->lat.cells[0] * sp->lat.cells[1] : sp->lat.cells[0];
+  const long long plane = (d == 3 ? (long long)sp->lat.nodes[0] * sp->lat.nodes[1] : sp->lat.nodes[0]) * d;
+  const long long n_planes = sp->lat.nodes[d - 1];
+  const int nl = sp->lat.cells[d - 1];
+  long long nt;
+  int cpt;
+  hf_tangent_tiles(op, &nt, &cpt);
+  std::vector<long long> cuts;
+  for (int k = 0; k <= chunks; ++k) {
+    const long long b = (long long)nl * k / chunks;
+    const long long c = std::min(nt, (b * layer + cpt - 1) / cpt);
+    if (cuts.empty() || c > cuts.back()) cuts.push_back(c);
+  }
+  auto planes = [&](long long t0, long long t1, long long& lo, long long& hi) {
+    const long long z0 = t0 * cpt / layer;
+    const long long z1 = (std::min(t1 * cpt, sp->lat.n_el) - 1) / layer;
+    lo = z0 * deg;
+    hi = (z1 + 1) * deg + 1;
+  };
+  const size_t need = 2 * cuts.size() + 4;
+  while (h->ev.size() < need) {
+    cudaEvent_t e;
+    HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->ev.push_back(e);
+  }
+  size_t ie = 0;
+  HF_CUDA(cudaEventRecord(h->ev[ie], h->cap));
+  HF_CUDA(cudaStreamWaitEvent(h->s_in, h->ev[ie], 0));
+  HF_CUDA(cudaStreamWaitEvent(h->s_out, h->ev[ie], 0));
+  ++ie;
+  long long copied = 0, filled = 0, sent = 0;
+  for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+    const long long t0 = cuts[k], t1 = cuts[k + 1];
+    long long lo, hi;
+    planes(t0, t1, lo, hi);
+    if (hi > copied) {
+      HF_CUDA(cudaMemcpyAsync(h->xd + copied * plane, xh + copied * plane, sizeof(double) * (hi - copied) * plane,
+                              cudaMemcpyHostToDevice, h->s_in));
+      copied = hi;
+      HF_CUDA(cudaEventRecord(h->ev[ie], h->s_in));
+      HF_CUDA(cudaStreamWaitEvent(h->cap, h->ev[ie], 0));
+      ++ie;
+    }
+    int mode = 0;
+    if (hi > filled) {
+      const long long off = filled * plane, cnt = (hi - filled) * plane;
+      k_fill_masked<double><<<vec_blocks(cnt), 256, 0, h->cap>>>(cnt, h->yd + off, h->xd + off, sp->d_mask + off, 0.0,
+                                                                 nullptr);
+      HF_CUDA(cudaGetLastError());
+      filled = hi;
+      mode = 1;  // programmatic dependent of the fill
+    }
+    const int rc = tangent_apply(op, h->xd, h->yd, nullptr, mode, h->cap, t0, t1);
+    if (rc != HF_OK) return rc;
+    long long fin = n_planes;
+    if (k + 2 < cuts.size()) {
+      long long nlo, nhi;
+      planes(cuts[k + 1], cuts[k + 2], nlo, nhi);
+      fin = nlo;
+    }
+    if (fin > sent) {
+      HF_CUDA(cudaEventRecord(h->ev[ie], h->cap));
+      HF_CUDA(cudaStreamWaitEvent(h->s_out, h->ev[ie], 0));
+      ++ie;
+      HF_CUDA(cudaMemcpyAsync(yh + sent * plane, h->yd + sent * plane, sizeof(double) * (fin - sent) * plane,
+                              cudaMemcpyDeviceToHost, h->s_out));
+      sent = fin;
+    }
+  }
+  HF_CUDA(cudaEventRecord(h->ev[ie], h->s_in));
+  HF_CUDA(cudaStreamWaitEvent(h->cap, h->ev[ie], 0));
+  ++ie;
+  HF_CUDA(cudaEventRecord(h->ev[ie], h->s_out));
+  HF_CUDA(cudaStreamWaitEvent(h->cap, h->ev[ie], 0));
+  return HF_OK;
+}
+
+HF_API int hf_host_register(void* p, long long bytes) {
+  if (!p || bytes <= 0) return fail(HF_ERR_ARG, "null or empty host range");
+  HF_CUDA(cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault));
+  return HF_OK;
+}
+
+HF_API int hf_host_unregister(void* p) {
+  if (!p) return fail(HF_ERR_ARG, "null host pointer");
+  HF_CUDA(cudaHostUnregister(p));
+  return HF_OK;
+}
+
+HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y_host, int chunks, void* stream) {
+  if (!op || !x_host || !y_host) return fail(HF_ERR_ARG, "null argument");
+  if (op->fp32) return fail(HF_ERR_UNSUPPORTED, "host apply of an fp32-storage tangent");
+  hf_space* sp = op->sp;
+  const long long bytes = (long long)sizeof(double) * sp->n_dofs;
+  if (sp->n_dofs == 0) return HF_OK;
+  if (!page_locked(x_host, bytes) || !page_locked(y_host, bytes))
+    return fail(HF_ERR_ARG, "host buffers must be page-locked (cudaHostAlloc, or hf_host_register)");
+  if (chunks < 1) chunks = 1;
+  if (chunks > sp->lat.cells[sp->dim - 1]) chunks = sp->lat.cells[sp->dim - 1];
+  if (sp->lat.n_el == 0) chunks = 1;
+  HostPipe* h = op->host;
+  if (!h) {
+    h = op->host = new HostPipe();
+    HF_CUDA(cudaMalloc((void**)&h->xd, bytes));
+    HF_CUDA(cudaMalloc((void**)&h->yd, bytes));
+    HF_CUDA(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+    HF_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    HF_CUDA(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+  }
+  HostPipe::Entry* hit = nullptr;
+  for (int i = 0; i < h->ng; ++i)
+    if (h->g[i].x == x_host && h->g[i].y == y_host && h->g[i].chunks == chunks) hit = &h->g[i];
+  if (!hit) {
+    cudaGraph_t graph;
+    HF_CUDA(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+    const int rc = host_pipe_enqueue(op, h, x_host, y_host, chunks);
+    const cudaError_t ce = cudaStreamEndCapture(h->cap, &graph);
+    if (rc != HF_OK) {
+      if (ce == cudaSuccess) cudaGraphDestroy(graph);
+      return rc;
+    }
+    HF_CUDA(ce);
+    cudaGraphExec_t exec;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    HF_CUDA(ie);
+    int slot = h->ng;
+    if (slot == HostPipe::NG) {  // evict the least recently used pipeline
+      slot = 0;
+      for (int i = 1; i < h->ng; ++i)
+        if (h->g[i].used < h->g[slot].used) slot = i;
+      cudaGraphExecDestroy(h->g[slot].exec);
+    } else {
+      ++h->ng;
+    }
+    h->g[slot] = {x_host, y_host, chunks, exec, 0};
+    hit = &h->g[slot];
+  }
+  hit->used = ++h->clock;
+  HF_CUDA(cudaGraphLaunch(hit->exec, S(stream)));
+  return HF_OK;
+}
+
 HF_API int hf_tangent_assemble_local(hf_tangent* op, double* vals_dev, void* stream) {
   if (!op || !vals_dev) return fail(HF_ERR_ARG, "null argument");
   if (op->strategy != HF_TENSOR4 || op->fp32)
@@ -563,6 +762,7 @@ HF_API int hf_tangent_storage(const hf_tangent* op, long long* storage_bytes, in
 
 HF_API int hf_tangent_destroy(hf_tangent* op) {
   if (!op) return HF_OK;
+  host_pipe_free(op->host);
   cudaFree(op->d_cache);
   cudaFree(op->d_ubar);
   delete op;

@@ -353,7 +353,7 @@ class MatrixFreeTangent:
         tensor in with a pinned ``out`` runs the host-to-host pipeline
         (``apply_host``)."""
         if (out is not None and isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned()
-                and out.is_pinned() and self.problem.mesh.n_elements >= 4096 and self.storage == "fp64"):
+                and out.is_pinned() and self.storage == "fp64"):
             return self.apply_host(x, out)
         xd = dv.as_dev(x)
         if self.storage == "fp32":  # the public apply stays fp64 in, fp64 out
@@ -370,69 +370,16 @@ class MatrixFreeTangent:
         return dv.like_input(y, x)
 
     def apply_host(self, xh: torch.Tensor, yh: torch.Tensor, chunks: int = 4) -> torch.Tensor:
-        """y = A x between pinned host buffers, pipelined over slabs of cell
-        layers: the H2D copy of the next slab's node planes, the cell kernel of
-        this slab (tile range) and the D2H copy of the planes no later slab
-        touches run on three streams.  Cells are lexicographic with the last
-        axis slowest, so a range of tiles touches a contiguous range of node
-        planes, i.e. a contiguous DoF range."""
-        p = self.problem
-        mesh = p.mesh
-        d, deg = p.dim, p.degree
-        n = p.n_dofs
-        layer = int(np.prod(mesh.cells[:-1]))
-        plane = int(np.prod([c * deg + 1 for c in mesh.cells[:-1]])) * d
-        n_planes = mesh.cells[-1] * deg + 1
-        nt, cpt = self.tiles()
-        n_el = mesh.n_elements
-        nl = mesh.cells[-1]
-        bounds = sorted({(nl * k) // chunks for k in range(chunks + 1)})
-        tile_cuts = [min(nt, -(-(b * layer) // cpt)) for b in bounds]
-        ranges = [(a, b) for a, b in zip(tile_cuts, tile_cuts[1:]) if b > a]
-
-        def planes(t0, t1):  # node planes touched by tiles [t0, t1)
-            z0 = (t0 * cpt) // layer
-            z1 = (min(t1 * cpt, n_el) - 1) // layer
-            return z0 * deg, (z1 + 1) * deg + 1  # [lo, hi)
-
-        dev = torch.device("cuda")
-        if getattr(self, "_host_bufs", None) is None or self._host_bufs[0].numel() != n:
-            self._host_bufs = (torch.empty(n, dtype=torch.float64, device=dev),
-                               torch.empty(n, dtype=torch.float64, device=dev),
-                               torch.cuda.Stream(), torch.cuda.Stream())
-        xd, yd, s_in, s_out = self._host_bufs
-        main = torch.cuda.current_stream()
-        s_in.wait_stream(main)
-        s_out.wait_stream(main)
-        L = lib()
-        mask = p.mask_ptr()
-        copied = filled = sent = 0  # planes [0, .) already copied in / filled / copied out
-        for k, (t0, t1) in enumerate(ranges):
-            lo, hi = planes(t0, t1)
-            if hi > copied:
-                with torch.cuda.stream(s_in):
-                    sl = slice(copied * plane, hi * plane)
-                    xd[sl].copy_(xh[sl], non_blocking=True)
-                copied = hi
-                ev = torch.cuda.Event()
-                ev.record(s_in)
-                main.wait_event(ev)
-            if hi > filled:
-                off, cnt = filled * plane, (hi - filled) * plane
-                check(L.hf_fill_masked(cnt, ct.c_void_p(yd.data_ptr() + 8 * off), ct.c_void_p(xd.data_ptr() + 8 * off),
-                                       ct.c_void_p(mask.value + off), 0.0, dv.stream()))
-                filled = hi
-            check(lib().hf_tangent_apply_tiles(self._op, dv.ptr(xd), dv.ptr(yd), None, t0, t1, 0, dv.stream()))
-            final = planes(*ranges[k + 1])[0] if k + 1 < len(ranges) else n_planes
-            if final > sent:
-                ev = torch.cuda.Event()
-                ev.record(main)
-                s_out.wait_event(ev)
-                with torch.cuda.stream(s_out):
-                    sl = slice(sent * plane, final * plane)
-                    yh[sl].copy_(yd[sl], non_blocking=True)
-                sent = final
-        s_out.synchronize()
+        """y = A x between page-locked host buffers (hf_tangent_apply_host): the
+        H2D copy of each slab's node planes, the slab's cell kernel and the D2H
+        copy of finished planes overlap on three streams; the pipeline is a
+        CUDA graph captured on first use per buffer pair and replayed after."""
+        if xh.dtype != torch.float64 or yh.dtype != torch.float64 or xh.numel() != self.n_dofs \
+                or yh.numel() != self.n_dofs or not (xh.is_contiguous() and yh.is_contiguous()):
+            raise ValueError("apply_host needs contiguous float64 host vectors of n_dofs entries")
+        check(lib().hf_tangent_apply_host(self._op, ct.c_void_p(xh.data_ptr()), ct.c_void_p(yh.data_ptr()), chunks,
+                                          dv.stream()))
+        torch.cuda.current_stream().synchronize()
         return yh
 
     def __call__(self, x):

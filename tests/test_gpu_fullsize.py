@@ -94,3 +94,45 @@ def test_pinned_host_apply_pipeline_matches_device_apply():
         op.apply(xh, out=yh)
         assert _rel(yh.cuda(), yd) < 1e-14
         assert torch.equal(yh[wl.fine.constraints.mask], xh[wl.fine.constraints.mask])
+
+
+@pytest.mark.parametrize("cfg,m", [(1, None), (2, 6), (3, 3)])
+def test_host_apply_graph_chunks_and_buffers(cfg, m):
+    """hf_tangent_apply_host: every slab count (incl. more slabs than cell
+    layers), new data through a cached graph, more buffer pairs than the graph
+    cache holds, and numpy memory page-locked with hf_host_register."""
+    import ctypes as ct
+
+    from paper_1904_13131_b200 import MatrixFreeTangent
+    from paper_1904_13131_b200._lib import HfError, check, lib
+    from paper_1904_13131_b200.workloads import make_workload
+
+    wl = make_workload(cfg, seed=5, m=m)
+    op = MatrixFreeTangent(wl.fine, wl.ubar, "tensor4")
+    n = op.n_dofs
+    pairs = [(torch.empty(n, dtype=torch.float64).pin_memory(), torch.empty(n, dtype=torch.float64).pin_memory())
+             for _ in range(6)]
+    rng = np.random.default_rng(11)
+    for rep in range(2):
+        for k, (xh, yh) in enumerate(pairs):
+            for chunks in (1, 3, 8, 1000):
+                xh.copy_(torch.from_numpy(rng.standard_normal(n)))
+                yh.fill_(np.nan)
+                op.apply_host(xh, yh, chunks=chunks)
+                yd = op.apply(xh.cuda())
+                assert _rel(yh.cuda(), yd) < 1e-14, (rep, k, chunks)
+    # pageable memory is refused, registered numpy memory accepted
+    xa = rng.standard_normal(n)
+    ya = np.zeros(n)
+    with pytest.raises(HfError):
+        check(lib().hf_tangent_apply_host(op._op, ct.c_void_p(xa.ctypes.data), ct.c_void_p(ya.ctypes.data), 4, None))
+    check(lib().hf_host_register(ct.c_void_p(xa.ctypes.data), xa.nbytes))
+    check(lib().hf_host_register(ct.c_void_p(ya.ctypes.data), ya.nbytes))
+    try:
+        check(lib().hf_tangent_apply_host(op._op, ct.c_void_p(xa.ctypes.data), ct.c_void_p(ya.ctypes.data), 4, None))
+        torch.cuda.synchronize()
+        yd = op.apply(torch.from_numpy(xa).cuda())
+        assert _rel(torch.from_numpy(ya).cuda(), yd) < 1e-14
+    finally:
+        check(lib().hf_host_unregister(ct.c_void_p(xa.ctypes.data)))
+        check(lib().hf_host_unregister(ct.c_void_p(ya.ctypes.data)))

@@ -21,7 +21,7 @@ def t(f, reps=20):
     e1.record(); torch.cuda.synchronize(); w1 = time.perf_counter()
     return e0.elapsed_time(e1) / reps * 1e3, (w1 - w0) / reps * 1e6
 print("plain   dev %.1f us  wall %.1f us" % t(plain))
-for ch in (1, 2, 4, 8):
+for ch in (1, 2, 4, 8, 16, 32):
     print(f"piped{ch}  dev %.1f us  wall %.1f us" % t(piped(ch)))
 # launch-only cost of apply_host (no sync): how long does the host take to enqueue?
 print("h2d only dev %.1f us wall %.1f" % t(lambda: xd.copy_(xh, non_blocking=True)))
