@@ -257,6 +257,11 @@ HF_API int hf_space_create(int dim, int degree, int nq1, const int* cells, const
   sp->lat.n_nodes = nn;
   sp->lat.n_qp = nel * nq;
   sp->n_dofs = nn * dim;
+  if (sp->n_dofs >= (1ll << 31)) {  // the cell kernels index DoFs in 32 bits
+    delete sp;
+    return fail(HF_ERR_UNSUPPORTED, "n_dofs must be < 2^31 on one device (partition the mesh over more GPUs)");
+  }
+  for (int a = 0; a < 2; ++a) hf_fastdiv_init((unsigned)sp->lat.cells[a], sp->lat.dm[a], sp->lat.ds[a]);
   cudaStream_t s = S(stream);
   long long nverts = 1;
   for (int a = 0; a < dim; ++a) nverts *= (cells[a] + 1);

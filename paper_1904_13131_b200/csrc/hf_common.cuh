@@ -50,7 +50,18 @@ struct HfLattice {
   long long n_el;
   long long n_nodes;
   long long n_qp;  // n_el * nq
+  // n / cells[a] for 0 <= n < 2^31 as (umulhi(n, dm[a]) + n) >> ds[a]
+  // (division by an invariant through a multiply; hf_fastdiv_init)
+  unsigned dm[2], ds[2];
 };
+
+inline void hf_fastdiv_init(unsigned d, unsigned& m, unsigned& s) {
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;  // l = ceil(log2 d)
+  m = (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+  s = l;
+}
+HF_DEV unsigned hf_fastdiv(unsigned n, unsigned m, unsigned s) { return (__umulhi(n, m) + n) >> s; }
 
 // ---- ordered-double atomics (min/max of doubles through uint64 atomics) ----
 HF_DEV unsigned long long hf_ord(double v) {

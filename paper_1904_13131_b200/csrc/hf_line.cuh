@@ -148,7 +148,7 @@ HF_DEV void line_map(int lane, int& slot, int& m, int& t, bool& act, LineOff<DIM
     m = slot / K::L;
     t = slot - m * K::L;
     int q[3][N] = {};
-    Z::offsets(slot, q);
+    Z::offsets(lane, q);
 #pragma unroll
     for (int a = 0; a < DIM; ++a)
 #pragma unroll
@@ -194,26 +194,29 @@ HF_DEV void c_line(const double (&M)[N][N], double (&v)[DIM][N]) {
   }
 }
 
-// first lattice node of cell e
+// First lattice node of cell e, and the first node and stride (in nodes) of
+// line t along the last axis.  32-bit index arithmetic: hf_space_create
+// guarantees n_dofs < 2^31; the cell coordinates come from multiply-shift
+// divisions by the invariant cell counts (HfLattice::dm/ds).
 template <int DIM>
-HF_DEV long long cell_node0(const HfLattice& lat, long long e, int degree) {
-  long long r = e;
-  const int ex = (int)(r % lat.cells[0]);
-  r /= lat.cells[0];
-  const int ey = (int)(r % lat.cells[1]);
-  const int ez = (DIM == 3) ? (int)(r / lat.cells[1]) : 0;
-  return (long long)ex * degree +
-         (long long)lat.nodes[0] * ((long long)ey * degree + (long long)lat.nodes[1] * ((long long)ez * degree));
+HF_DEV unsigned cell_node0(const HfLattice& lat, unsigned e, int degree) {
+  const unsigned r = hf_fastdiv(e, lat.dm[0], lat.ds[0]);
+  const unsigned ex = e - r * (unsigned)lat.cells[0];
+  unsigned ey = r, ez = 0;
+  if (DIM == 3) {
+    ez = hf_fastdiv(r, lat.dm[1], lat.ds[1]);
+    ey = r - ez * (unsigned)lat.cells[1];
+  }
+  return (ex + (unsigned)lat.nodes[0] * (ey + (unsigned)lat.nodes[1] * ez)) * (unsigned)degree;
 }
 
-// first node and stride (in nodes) of line t along the last axis
 template <int DIM, int N>
-HF_DEV void last_axis_line(const HfLattice& lat, long long node0, int t, long long& nb, long long& s_last) {
-  const int i = t % N;
-  const int j = DIM == 3 ? t / N : 0;
-  const long long sy = lat.nodes[0];
-  s_last = DIM == 3 ? sy * lat.nodes[1] : sy;
-  nb = node0 + i + (DIM == 3 ? j * sy : 0);
+HF_DEV void last_axis_line(const HfLattice& lat, unsigned node0, int t, unsigned& nb, unsigned& s_last) {
+  const unsigned i = (unsigned)(t % N);
+  const unsigned j = DIM == 3 ? (unsigned)(t / N) : 0u;
+  const unsigned sy = (unsigned)lat.nodes[0];
+  s_last = DIM == 3 ? sy * (unsigned)lat.nodes[1] : sy;
+  nb = node0 + i + (DIM == 3 ? j * sy : 0u);
 }
 
 // The last-axis line of one tile gathered ahead of use (software pipelining
@@ -224,7 +227,7 @@ struct Gather {  // values held in fp64 whatever the storage type
   double u[DIM][N];
   double ub[DIM][N];  // scalar strategy only
   unsigned mb;
-  long long e, node0;
+  unsigned e, node0;
   bool live;
 };
 
@@ -233,24 +236,25 @@ HF_DEV void gather_tile(const LineArgs& a, long long tile, long long ntiles, int
                         Gather<DIM, N, VAR>& g) {
   using K = LineCfg<DIM, N>;
   const ST* xs = reinterpret_cast<const ST*>(a.x);  // fp64, or fp32 vectors of a mixed-precision level
-  g.e = tile * K::CPW + m;
-  g.live = act && tile < ntiles && g.e < a.lat.n_el;
+  const long long e = tile * K::CPW + m;
+  g.live = act && tile < ntiles && e < a.lat.n_el;
+  g.e = (unsigned)e;
   g.mb = 0;
-  g.node0 = g.live ? cell_node0<DIM>(a.lat, g.e, a.degree) : 0;
+  g.node0 = g.live ? cell_node0<DIM>(a.lat, g.e, a.degree) : 0u;
   if (!g.live) return;
-  long long nb, s_last;
+  unsigned nb, s_last;
   last_axis_line<DIM, N>(a.lat, g.node0, t, nb, s_last);
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    const long long d0 = (nb + l * s_last) * DIM;
-    HF_ASSERT(d0 >= 0 && d0 + DIM <= a.lat.n_nodes * DIM);
+    const unsigned d0 = (nb + l * s_last) * DIM;
+    HF_ASSERT((long long)d0 + DIM <= a.lat.n_nodes * DIM);
 #pragma unroll
     for (int c = 0; c < DIM; ++c) {
       g.u[c][l] = (double)__ldg(xs + d0 + c);
       if (VAR == SCALAR) g.ub[c][l] = __ldg(a.ubar + d0 + c);
     }
   }
-  g.mb = __ldg(a.lmask + g.e * K::L + t);
+  g.mb = __ldg(a.lmask + (g.e * (unsigned)K::L + (unsigned)t));
 }
 
 // Unit-cell gradients of the nodal line values u0 (last axis, already masked)
@@ -618,12 +622,12 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       double v[DIM][N];
       ld_line<DIM, N, DIM - 1>(Q, lo, v);
       c_line<DIM, N, true>(T.V, v);
-      long long nb, s_last;
+      unsigned nb, s_last;
       last_axis_line<DIM, N>(a.lat, g.node0, t, nb, s_last);
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        const long long d0 = (nb + l * s_last) * DIM;
-        HF_ASSERT(d0 >= 0 && d0 + DIM <= a.lat.n_nodes * DIM);
+        const unsigned d0 = (nb + l * s_last) * DIM;
+        HF_ASSERT((long long)d0 + DIM <= a.lat.n_nodes * DIM);
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc)
           if (!((g.mb >> (cc * N + l)) & 1u)) atomicAdd(reinterpret_cast<ST*>(a.y) + d0 + cc, (ST)v[cc][l]);

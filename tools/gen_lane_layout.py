@@ -106,13 +106,30 @@ def emit(f, n, comp, lane_slot, off):
     f.write(f"  static constexpr int COMP = {comp};  // doubles per component block of a warp's line buffer\n")
     f.write("  // slot of each lane as 5-bit fields of three immediates (31 = idle): no memory access\n")
     f.write("  static constexpr unsigned long long B0 = 0x%xull, B1 = 0x%xull, B2 = 0x%xull;\n" % tuple(words))
-    f.write("  // buffer offset of the site at position l along axis a of the slot's line: a divergent\n"
-            "  // switch of immediates once per thread, no memory access\n")
-    f.write(f"  __device__ __forceinline__ static void offsets(int slot, int (&o)[3][{n}]) {{\n    switch (slot) {{\n")
-    for sl in range(len(off)):
-        vals = "; ".join(f"o[{a}][{l}] = {off[sl][a][l]}" for a in range(3) for l in range(n))
-        f.write(f"      case {sl}: {vals}; break;\n")
-    f.write("      default: break;\n    }\n  }\n};\n\n")
+    bits = max(1, (comp - 1).bit_length())
+    per = 64 // bits
+    nw = -(-3 * n // per)
+    table = []
+    for lane, sl in enumerate(lane_slot):
+        w = [0] * nw
+        if sl >= 0:
+            for k, v in enumerate(off[sl][a][l] for a in range(3) for l in range(n)):
+                w[k // per] |= v << (bits * (k % per))
+        table.append(w)
+    f.write(f"  // buffer offset of the site at position l along axis a of the lane's line: {bits}-bit fields\n"
+            f"  // of a per-lane table (one coalesced load per thread at kernel start)\n")
+    f.write(f"  static constexpr int OFF_BITS = {bits}, OFF_WORDS = {nw};\n")
+    f.write(f"  __device__ __forceinline__ static void offsets(int lane, int (&o)[3][{n}]);\n}};\n")
+    f.write(f"static __device__ const unsigned long long kLaneOff3_{n}[32][{nw}] = {{\n")
+    for lane, w in enumerate(table):
+        f.write("    {" + ", ".join(f"0x{v:x}ull" for v in w) + f"}},  // lane {lane}\n")
+    f.write("};\n")
+    f.write(f"__device__ __forceinline__ void LaneMapT<3, {n}>::offsets(int lane, int (&o)[3][{n}]) {{\n"
+            f"  unsigned long long w[{nw}];\n"
+            f"#pragma unroll\n  for (int i = 0; i < {nw}; ++i) w[i] = __ldg(&kLaneOff3_{n}[lane][i]);\n"
+            f"#pragma unroll\n  for (int k = 0; k < {3 * n}; ++k)\n"
+            f"    o[k / {n}][k % {n}] = (int)((w[k / {per}] >> ({bits} * (k % {per}))) & {(1 << bits) - 1}ull);\n"
+            "}\n\n")
 
 
 def main():
