@@ -222,6 +222,18 @@ HF_API int hf_cg_update_p(long long n, double* p, const double* z, const double*
 /* z = inv_d r; out_dev[0] = r . z */
 HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, const double* inv_d, double* out_dev,
                          void* stream);
+/* Jacobi-PCG / Lanczos range estimate with device-side scalars
+ * (estimate_eigenvalue_range, multigrid.py:112-166): no host round trip per
+ * iteration.  scal_dev[4]: [0] rz = r.z (set by hf_jacobi_dot before
+ * hf_lanczos_init), [1] pAp, [2] rz_new, [3] beta; state_dev[2]: [0] stop
+ * flag, [1] steps recorded; ab_dev[2k] = alpha_k, ab_dev[2k+1] = beta_k.
+ * hf_lanczos_init applies the reference's rz > 0 / finite test; each
+ * hf_lanczos_step, after ap = A p (skipped while state_dev[0] != 0, e.g.
+ * hf_tangent_apply_flagged), does pAp, r -= alpha ap, z = inv_d r, rz_new,
+ * the pAp <= 0 / rz_new <= 1e-28 rz / finite tests and p = z + beta p. */
+HF_API int hf_lanczos_init(const double* scal_dev, int* state_dev, void* stream);
+HF_API int hf_lanczos_step(hf_ws* w, long long n, double* r, double* z, double* p, const double* ap,
+                           const double* inv_d, double* scal_dev, double* ab_dev, int* state_dev, void* stream);
 /* diagnostic: blocks x threads threads run 8 independent chains of `iters`
  * DFMAs (16 * iters flops per thread) -- the measured fp64 roofline peak */
 HF_API int hf_probe_dfma(long long iters, int blocks, int threads, double* sink_dev, void* stream);

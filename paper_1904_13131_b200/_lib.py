@@ -81,6 +81,8 @@ _SIGS = {
     "hf_cg_update_p": (I, [LL, P, P, P, I, I, P]),
     "hf_jacobi_dot": (I, [P, LL, P, P, P, P, P]),
     "hf_axpby": (I, [LL, D, P, D, P, P]),
+    "hf_lanczos_init": (I, [P, P, P]),
+    "hf_lanczos_step": (I, [P, LL, P, P, P, P, P, P, P, P, P]),
     "hf_fill_masked_f32": (I, [LL, P, P, P, D, P]),
     "hf_cheb_step_f32": (I, [LL, P, P, P, P, P, I, D, D, D, I, P, P, P, P]),
     "hf_resid_masked_f32": (I, [LL, P, P, P, P, P]),

@@ -1090,6 +1090,27 @@ HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, cons
   return HF_OK;
 }
 
+HF_API int hf_lanczos_init(const double* scal_dev, int* state_dev, void* stream) {
+  if (!scal_dev || !state_dev) return fail(HF_ERR_ARG, "null argument");
+  k_lanczos_init<<<1, 1, 0, S(stream)>>>(scal_dev, state_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_lanczos_step(hf_ws* w, long long n, double* r, double* z, double* p, const double* ap,
+                           const double* inv_d, double* scal_dev, double* ab_dev, int* state_dev, void* stream) {
+  if (!w || !r || !z || !p || !ap || !inv_d || !scal_dev || !ab_dev || !state_dev)
+    return fail(HF_ERR_ARG, "null argument");
+  cudaStream_t s = S(stream);
+  k_dot<<<red_blocks(n), RED_THREADS, 0, s>>>(n, p, ap, w->d_partials, w->d_counter, scal_dev + 1, state_dev);
+  k_lanczos_r<<<vec_blocks(n), 256, 0, s>>>(n, r, ap, scal_dev, state_dev);
+  k_jacobi_dot<<<red_blocks(n), RED_THREADS, 0, s>>>(n, z, r, inv_d, w->d_partials, w->d_counter, scal_dev + 2);
+  k_lanczos_scalar<<<1, 1, 0, s>>>(scal_dev, state_dev, ab_dev);
+  k_lanczos_p<<<vec_blocks(n), 256, 0, s>>>(n, p, z, scal_dev, state_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
 HF_API int hf_axpby(long long n, double a, const double* x, double b, double* y, void* stream) {
   if (!x || !y) return fail(HF_ERR_ARG, "null argument");
   k_axpby<<<vec_blocks(n), 256, 0, S(stream)>>>(n, a, x, b, y);

@@ -195,6 +195,56 @@ __global__ void k_jacobi_dot(long long n, double* __restrict__ z, const double* 
 }
 
 // y = a x + b y  (general axpby)
+// ---- Jacobi-PCG / Lanczos range estimate with device-side scalars
+// (estimate_eigenvalue_range, multigrid.py:112-166).  scal: [0] rz, [1] pAp,
+// [2] rz_new, [3] beta; st: [0] stop flag, [1] recorded steps; ab[2k] alpha_k,
+// ab[2k+1] beta_k.  No host round trip per iteration.
+__global__ void k_lanczos_r(long long n, double* __restrict__ r, const double* __restrict__ ap, const double* scal,
+                            const int* st) {
+  if (st[0] || scal[1] <= 0.0) return;
+  const double a = -(scal[0] / scal[1]);  // r -= alpha ap
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    r[i] = fma(a, ap[i], r[i]);
+}
+
+// one thread: the reference's tests and recording after r.z (rz_new) is known
+__global__ void k_lanczos_scalar(double* scal, int* st, double* ab) {
+  if (st[0]) return;
+  const double rz = scal[0], pap = scal[1], rzn = scal[2];
+  const int k = st[1];
+  if (pap <= 0.0) {  // multigrid.py: break before recording
+    st[0] = 1;
+    return;
+  }
+  const double alpha = rz / pap;
+  ab[2 * k] = alpha;
+  st[1] = k + 1;
+  if (rzn <= 1e-28 * rz || !isfinite(rzn)) {
+    st[0] = 1;
+    return;
+  }
+  const double beta = rzn / rz;
+  ab[2 * k + 1] = beta;
+  scal[0] = rzn;
+  scal[3] = beta;
+}
+
+// p = z + beta p
+__global__ void k_lanczos_p(long long n, double* __restrict__ p, const double* __restrict__ z, const double* scal,
+                            const int* st) {
+  if (st[0]) return;
+  const double b = scal[3];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = fma(b, p[i], z[i]);
+}
+
+// st[0] = !(rz > 0 and finite), st[1] = 0 (the check before the first iteration)
+__global__ void k_lanczos_init(const double* scal, int* st) {
+  const double rz = scal[0];
+  st[0] = (rz <= 0.0 || !isfinite(rz)) ? 1 : 0;
+  st[1] = 0;
+}
+
 __global__ void k_axpby(long long n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     y[i] = a * x[i] + (b == 0.0 ? 0.0 : b * y[i]);

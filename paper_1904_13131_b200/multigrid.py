@@ -115,60 +115,25 @@ def restrict_solution(problems: list[Problem], u_fine, keep_constrained: bool = 
 _RHS_CACHE: dict = {}
 
 
-def _lanczos_rhs(n: int, seed: int, mask: np.ndarray | None) -> torch.Tensor:
-    """b = default_rng(seed).standard_normal(n), constrained = 0 (multigrid.py:121-124), cached on device."""
-    key = (n, seed, None if mask is None else hash(mask.tobytes()))
+def _lanczos_rhs(n: int, seed: int, mask) -> torch.Tensor:
+    """b = default_rng(seed).standard_normal(n), constrained = 0 (multigrid.py:121-124).  The
+    unmasked draw is cached on the device per (n, seed); the mask (numpy or device bool) is
+    applied on the device."""
+    key = (n, seed)
     if key not in _RHS_CACHE:
-        b = np.random.default_rng(seed).standard_normal(n)
-        if mask is not None:
-            b[mask] = 0.0
-        _RHS_CACHE[key] = dv.as_dev(b)
-    return _RHS_CACHE[key]
+        _RHS_CACHE[key] = dv.as_dev(np.random.default_rng(seed).standard_normal(n))
+    b = _RHS_CACHE[key]
+    if mask is None:
+        return b.clone()
+    m = mask if isinstance(mask, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(mask, dtype=bool))
+    return b.masked_fill(m.to(device=b.device, dtype=torch.bool), 0.0)
 
 
-def estimate_eigenvalue_range(apply_fn, diagonal, seed: int = 0, iterations: int = 30,
-                              constrained: np.ndarray | None = None) -> tuple[float, float]:
-    """Smallest and largest Ritz values of D^-1 A from a Jacobi-PCG/Lanczos run
-    (multigrid.py:112-166).  Vector work and dots on the device; the k x k
-    tridiagonal eigenproblem on the host with the reference's scipy call."""
-    diag = dv.as_dev(diagonal)
-    n = diag.numel()
-    b = _lanczos_rhs(n, seed, constrained)
-    inv_d = torch.reciprocal(diag)
-    r = b.clone()
-    z = torch.empty_like(r)
-    ap = torch.empty_like(r)
-    scal = torch.zeros(4, dtype=torch.float64, device="cuda")
-    ws = dv.Workspace.get().handle
-    L = lib()
-    check(L.hf_jacobi_dot(ws, n, dv.ptr(z), dv.ptr(r), dv.ptr(inv_d), dv.ptr(scal[0:1]), dv.stream()))
-    p = z.clone()
-    rz = float(scal[0].item())
-    alphas: list[float] = []
-    betas: list[float] = []
-    for _ in range(iterations):
-        if rz <= 0.0 or not np.isfinite(rz):
-            break
-        _apply_into(apply_fn, p, ap)
-        dv.dot(p, ap, scal[1:2])
-        pap = float(scal[1].item())
-        if pap <= 0.0:
-            break
-        alpha = rz / pap
-        check(L.hf_axpby(n, -alpha, dv.ptr(ap), 1.0, dv.ptr(r), dv.stream()))
-        check(L.hf_jacobi_dot(ws, n, dv.ptr(z), dv.ptr(r), dv.ptr(inv_d), dv.ptr(scal[2:3]), dv.stream()))
-        rz_new = float(scal[2].item())
-        if rz_new <= 1e-28 * rz or not np.isfinite(rz_new):
-            alphas.append(alpha)
-            break
-        beta = rz_new / rz
-        alphas.append(alpha)
-        betas.append(beta)
-        check(L.hf_axpby(n, 1.0, dv.ptr(z), beta, dv.ptr(p), dv.stream()))
-        rz = rz_new
-    if not alphas:
-        return 1.0, 1.0
+def _ritz_extremes(alphas, betas) -> tuple[float, float]:
+    """Extreme eigenvalues of the Lanczos tridiagonal (multigrid.py:156-166)."""
     k = len(alphas)
+    if k == 0:
+        return 1.0, 1.0
     diag_t = np.empty(k)
     diag_t[0] = 1.0 / alphas[0]
     for i in range(1, k):
@@ -178,6 +143,44 @@ def estimate_eigenvalue_range(apply_fn, diagonal, seed: int = 0, iterations: int
         return float(diag_t[0]), float(diag_t[0])
     ritz = scipy.linalg.eigvalsh_tridiagonal(diag_t, off_t)
     return float(ritz[0]), float(ritz[-1])
+
+
+def lanczos_coefficients(apply_fn, diagonal, seed: int = 0, iterations: int = 30, constrained=None):
+    """alpha_k, beta_k of the Jacobi-PCG run of estimate_eigenvalue_range
+    (multigrid.py:112-155).  All iterations are enqueued without a host round
+    trip: the scalars, the stopping tests and the recording live on the device
+    (hf_lanczos_step); the application is skipped once the run has stopped.
+    One synchronisation at the end reads the coefficients."""
+    diag = dv.as_dev(diagonal)
+    n = diag.numel()
+    r = _lanczos_rhs(n, seed, constrained)
+    inv_d = torch.reciprocal(diag)
+    z = torch.empty_like(r)
+    ap = torch.empty_like(r)
+    scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+    st = torch.zeros(2, dtype=torch.int32, device="cuda")
+    ab = torch.zeros(2 * max(iterations, 1), dtype=torch.float64, device="cuda")
+    ws = dv.Workspace.get().handle
+    L = lib()
+    check(L.hf_jacobi_dot(ws, n, dv.ptr(z), dv.ptr(r), dv.ptr(inv_d), dv.ptr(scal[0:1]), dv.stream()))
+    p = z.clone()
+    check(L.hf_lanczos_init(dv.ptr(scal), dv.ptr(st), dv.stream()))
+    for _ in range(iterations):
+        _apply_into(apply_fn, p, ap, st)
+        check(L.hf_lanczos_step(ws, n, dv.ptr(r), dv.ptr(z), dv.ptr(p), dv.ptr(ap), dv.ptr(inv_d), dv.ptr(scal),
+                                dv.ptr(ab), dv.ptr(st), dv.stream()))
+    k = int(st[1].item())
+    abh = ab[: 2 * k].cpu().numpy()
+    return abh[0::2].copy(), abh[1::2][: max(k - 1, 0)].copy()
+
+
+def estimate_eigenvalue_range(apply_fn, diagonal, seed: int = 0, iterations: int = 30,
+                              constrained=None) -> tuple[float, float]:
+    """Smallest and largest Ritz values of D^-1 A from a Jacobi-PCG/Lanczos run
+    (multigrid.py:112-166).  Vector work, dots and the stopping tests on the
+    device; the k x k tridiagonal eigenproblem on the host with the reference's
+    scipy call."""
+    return _ritz_extremes(*lanczos_coefficients(apply_fn, diagonal, seed, iterations, constrained))
 
 
 def estimate_lambda_max(apply_fn, diagonal, seed=0, iterations=30, constrained=None) -> float:
@@ -281,12 +284,17 @@ class LevelOperator:
             raise NonPositiveJacobian(f"level {level}: {err}", element=err.element, level=level) from err
         self.diag = self.op.diagonal()
         self.inv_diag = torch.reciprocal(self.diag)
-        mask = problem.constraints.mask
-        self.lam_min, self.lam_max = estimate_eigenvalue_range(self.op, self.diag, seed=seed, constrained=mask)
+        mask = problem.mask_dev
         if is_coarsest:
-            lo, _ = estimate_eigenvalue_range(self.op, self.diag, seed=seed, iterations=min(problem.n_dofs, 120),
-                                              constrained=mask)
+            # the 30-iteration run the reference does first is the prefix of the
+            # longer run (same RHS, same operations), so one run yields both
+            al, be = lanczos_coefficients(self.op, self.diag, seed=seed, iterations=max(min(problem.n_dofs, 120), 30),
+                                          constrained=mask)
+            self.lam_min, self.lam_max = _ritz_extremes(al[:30], be[:29])
+            lo, _ = _ritz_extremes(al[:min(problem.n_dofs, 120)], be[:min(problem.n_dofs, 120) - 1])
             self.lam_min = min(self.lam_min, lo)
+        else:
+            self.lam_min, self.lam_max = estimate_eigenvalue_range(self.op, self.diag, seed=seed, constrained=mask)
         dtype = torch.float64
         if precision == "fp32":
             self.op = MatrixFreeTangent(problem, u_level, strategy, storage="fp32")
