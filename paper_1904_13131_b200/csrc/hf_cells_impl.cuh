@@ -41,14 +41,23 @@ cudaError_t launch_apply_line_t(const CellArgs& c, cudaStream_t s) {
   const long long all_tiles = (c.lat.n_el + K::CPW - 1) / K::CPW;
   a.tile0 = c.tile1 < 0 ? 0 : c.tile0;
   a.tile1 = c.tile1 < 0 ? all_tiles : (c.tile1 < all_tiles ? c.tile1 : all_tiles);
-  TabLine<N> T;
+  TabLine<N> T = {};
   for (int l = 0; l < N; ++l)
     for (int o = 0; o < N; ++o) {
       T.V[l][o] = c.tab.V[l * N + o];
       T.Dc[l][o] = c.tab.Dc[l * N + o];
     }
+  if constexpr (LaneMapT<DIM, N>::ENABLED) {
+    using Z = LaneMapT<DIM, N>;
+    static_assert(Z::OFF_WORDS <= 2, "TabLine::loff holds two words per lane");
+    for (int lane = 0; lane < 32; ++lane)
+      for (int i = 0; i < Z::OFF_WORDS; ++i) T.loff[lane][i] = Z::TABLE[lane][i];
+  }
+  // One block per tile up to the resident capacity: a small level (fewer
+  // tiles than SMs) runs one warp per SM instead of W warps sharing a few SMs,
+  // which shortens its latency chain; larger levels fill every SM.
   const long long tiles = a.tile1 - a.tile0;
-  long long nb = (tiles + PL::W - 1) / PL::W;
+  long long nb = tiles;
   if (nb > resident) nb = resident;
   if (nb <= 0) return cudaSuccess;
   if (!c.fill) {

@@ -51,6 +51,9 @@ template <int N>
 struct TabLine {
   double V[N][N];   // V[l][o]  = N_l(xi_o)
   double Dc[N][N];  // Dc[l][o] = collocation derivative at Gauss point o of Gauss-basis l
+  // per-lane packed site offsets of a generated conflict-free layout
+  // (LaneMapT::TABLE); read from the constant bank with a per-lane index
+  unsigned long long loff[32][2];
 };
 
 struct LineArgs {
@@ -136,7 +139,7 @@ struct LineOff {
 
 // lane -> (slot = cell * L + line, cell m, line t, active) and its site offsets
 template <int DIM, int N>
-HF_DEV void line_map(int lane, int& slot, int& m, int& t, bool& act, LineOff<DIM, N>& o) {
+HF_DEV void line_map(int lane, const TabLine<N>& T, int& slot, int& m, int& t, bool& act, LineOff<DIM, N>& o) {
   using K = LineCfg<DIM, N>;
   using Y = LineLay<DIM, N>;
   if constexpr (LineMap<DIM, N>::CUSTOM) {
@@ -147,12 +150,13 @@ HF_DEV void line_map(int lane, int& slot, int& m, int& t, bool& act, LineOff<DIM
     slot = act ? sl : 0;
     m = slot / K::L;
     t = slot - m * K::L;
-    int q[3][N] = {};
-    Z::offsets(lane, q);
+    constexpr int per = 64 / Z::OFF_BITS;
+    unsigned long long ow[Z::OFF_WORDS];
 #pragma unroll
-    for (int a = 0; a < DIM; ++a)
+    for (int i = 0; i < Z::OFF_WORDS; ++i) ow[i] = T.loff[lane][i];
 #pragma unroll
-      for (int l = 0; l < N; ++l) o.off[a][l] = q[a < 3 ? a : 0][l];
+    for (int k = 0; k < DIM * N; ++k)
+      o.off[k / N][k % N] = (int)((ow[k / per] >> (Z::OFF_BITS * (k % per))) & ((1ull << Z::OFF_BITS) - 1));
   } else {
     act = lane < K::LANES;
     m = act ? lane / K::L : 0;
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   int slot, m, t;
   bool act;
   LineOff<DIM, N> lo;
-  line_map<DIM, N>(lane, slot, m, t, act, lo);
+  line_map<DIM, N>(lane, T, slot, m, t, act, lo);
   double* wb = lbuf + (size_t)warp * NB * Y::BUF;
   double* bufs[NB];
 #pragma unroll

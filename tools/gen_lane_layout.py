@@ -116,20 +116,14 @@ def emit(f, n, comp, lane_slot, off):
             for k, v in enumerate(off[sl][a][l] for a in range(3) for l in range(n)):
                 w[k // per] |= v << (bits * (k % per))
         table.append(w)
-    f.write(f"  // buffer offset of the site at position l along axis a of the lane's line: {bits}-bit fields\n"
-            f"  // of a per-lane table (one coalesced load per thread at kernel start)\n")
+    f.write(f"  // buffer offset of the site at position l along axis a of the lane's line: {bits}-bit\n"
+            f"  // fields of a per-lane table that the launcher passes as a kernel parameter\n"
+            f"  // (TabLine::loff: constant bank, no memory round trip at kernel start)\n")
     f.write(f"  static constexpr int OFF_BITS = {bits}, OFF_WORDS = {nw};\n")
-    f.write(f"  __device__ __forceinline__ static void offsets(int lane, int (&o)[3][{n}]);\n}};\n")
-    f.write(f"static __device__ const unsigned long long kLaneOff3_{n}[32][{nw}] = {{\n")
+    f.write(f"  static constexpr unsigned long long TABLE[32][{nw}] = {{\n")
     for lane, w in enumerate(table):
-        f.write("    {" + ", ".join(f"0x{v:x}ull" for v in w) + f"}},  // lane {lane}\n")
-    f.write("};\n")
-    f.write(f"__device__ __forceinline__ void LaneMapT<3, {n}>::offsets(int lane, int (&o)[3][{n}]) {{\n"
-            f"  unsigned long long w[{nw}];\n"
-            f"#pragma unroll\n  for (int i = 0; i < {nw}; ++i) w[i] = __ldg(&kLaneOff3_{n}[lane][i]);\n"
-            f"#pragma unroll\n  for (int k = 0; k < {3 * n}; ++k)\n"
-            f"    o[k / {n}][k % {n}] = (int)((w[k / {per}] >> ({bits} * (k % {per}))) & {(1 << bits) - 1}ull);\n"
-            "}\n\n")
+        f.write("      {" + ", ".join(f"0x{v:x}ull" for v in w) + f"}},  // lane {lane}\n")
+    f.write("  };\n};\n\n")
 
 
 def main():
