@@ -415,10 +415,80 @@ def _extras(args, hbm, prob, ubar, x, y, flush, nqp):
     nq3 = p3.mesh.n_elements * p3.n_qpoints_per_cell
     out["cfg3_q4"] = {s: variant(p3, wl3.ubar, x3, y3, s, nq3) for s in ("tensor4", "tensor2", "scalar")}
     out["matrix_based"] = _matrix_based(prob, ubar, x, flush, hbm)
+    out["cfg1"] = _cfg1(cpu=not args.no_cpu)
     if not args.no_newton:
         out["newton"] = _newton_iteration()
         out["newton_fp32_levels"] = _newton_iteration("fp32")
     return out
+
+
+def _cfg1(cpu: bool):
+    """Config 1 (BASELINE configs[0]): 2D 32^2 Q2 plane strain, GMG levels 4..32,
+    amplitude 0.005.  One tensor4 vmult on the seeded N(0,1) vector,
+    and one GMG-preconditioned CG solve of b = A x (constrained entries 0) to
+    rtol 1e-8 with the degree-4 Chebyshev smoother; GMG build + solve run
+    twice, the warm run reported.  With ``cpu``, the oracle port of the same
+    setup and solve on one host core beside it (the reference pkg "runs this
+    directly"; SURVEY P5 measured 0.9 s setup + 6.8 s solve)."""
+    import torch
+
+    from paper_1904_13131_b200 import MatrixFreeTangent, build_gmg, build_transfers, cg
+    from paper_1904_13131_b200.workloads import AMP_SOLVE, make_workload
+
+    wl = make_workload(1, seed=0, levels=True, amp=AMP_SOLVE)
+    probs = wl.problems
+    fine = probs[-1]
+    u = torch.from_numpy(wl.ubar).cuda()
+    x = torch.from_numpy(wl.x).cuda()
+    op = MatrixFreeTangent(fine, u, "tensor4")
+    y = torch.empty_like(x)
+    for _ in range(20):
+        op.apply_into(x, y)
+    reps = 200
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        op.apply_into(x, y)
+    e1.record()
+    torch.cuda.synchronize()
+    vm_ms = e0.elapsed_time(e1) / reps
+    b = op.apply(x)
+    b[fine.mask_dev] = 0.0
+    transfers = build_transfers(probs)
+    rec = None
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gmg = build_gmg(probs, u, "tensor4", seed=0, transfers=transfers)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        _, rep = cg(op, b, rel_tol=1e-8, preconditioner=gmg)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        rec = {"workload": "cfg1 2D 32^2 Q2 (8,450 DoFs), levels 4..32, tensor4, GMG-CG rtol 1e-8",
+               "n_dofs": fine.n_dofs, "vmult_ms": vm_ms, "vmult_GDoF_s": fine.n_dofs / vm_ms / 1e6,
+               "vmult_note": f"mean of {reps} back-to-back applies (the 2.9 MB working set is L2-resident)",
+               "gmg_setup_s": t1 - t0, "cg_solve_s": t2 - t1, "cg_iterations": rep.iterations,
+               "s_per_cg_iteration": (t2 - t1) / max(rep.iterations, 1)}
+        del gmg
+    if cpu:
+        from threadpoolctl import threadpool_limits
+
+        from oracle import hf_oracle as O
+
+        bh = b.cpu().numpy()
+        with threadpool_limits(1):
+            oprobs = [O.OProblem(2, 2, p.mesh.cells, p.mesh.vertices, p.mu_el, p.lam_el, p.constraints.mask)
+                      for p in probs]
+            t0 = time.perf_counter()
+            og = O.GMG(oprobs, wl.ubar, "tensor4", 0)
+            ot = O.Tangent(oprobs[-1], wl.ubar, "tensor4")
+            t1 = time.perf_counter()
+            _, its, _ = O.cg(ot.apply, bh, rel_tol=1e-8, preconditioner=og.apply)
+            t2 = time.perf_counter()
+        rec["cpu_port"] = {"gmg_setup_s": t1 - t0, "cg_solve_s": t2 - t1, "cg_iterations": its, "cores": 1,
+                           "kind": "port", "sample": "oracle numpy port of build_gmg + cg at cfg1, one solve"}
+    return rec
 
 
 def _matrix_based(prob, ubar, x, flush, hbm):

@@ -52,6 +52,7 @@ typedef struct hf_space hf_space;       /* one discretisation level (Problem)  *
 typedef struct hf_tangent hf_tangent;   /* MatrixFreeTangent                   */
 typedef struct hf_transfer hf_transfer; /* TransferOperator                    */
 typedef struct hf_ws hf_ws;             /* reduction workspace (one per stream) */
+typedef struct hf_coarse hf_coarse;     /* assembled coarsest-level operator    */
 
 typedef struct {
   int code;          /* HF_ERR_JACOBIAN when det F <= 0                        */
@@ -222,6 +223,23 @@ HF_API int hf_cg_update_p(long long n, double* p, const double* z, const double*
 /* z = inv_d r; out_dev[0] = r . z */
 HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, const double* inv_d, double* out_dev,
                          void* stream);
+/* ---- coarse_solve (multigrid.py:255-306) as one persistent kernel ----
+ * hf_coarse_create copies the CSR (int32 row pointers / columns, fp64 values)
+ * of the coarsest level's assembled tangent, with constrained rows and columns
+ * cleared and a unit diagonal (AssembledTangent, operators.py:481-490), i.e.
+ * the matrix-free apply's zero-in / identity-out operator.
+ * hf_coarse_cheb_solve runs the continuous Chebyshev iteration of
+ * _coarse_solve_into in one cooperative launch: x = inv_d b / theta, then up to
+ * max_applications - 1 further applications with the residual test
+ * ||b - A x|| <= rel_target ||b|| every `degree`-th application; scal_dev[0..2]
+ * = ||b||^2, target, last ||b - A x||^2; *flag_dev = 1 if it stopped on the
+ * test (or b == 0), 0 if it hit the cap.  d is scratch.  Graph-capturable. */
+HF_API int hf_coarse_create(long long n, long long nnz, const int* rowptr_dev, const int* col_dev,
+                            const double* val_dev, void* stream, hf_coarse** out);
+HF_API int hf_coarse_cheb_solve(hf_coarse* c, const double* b, double* x, double* d, const double* inv_d,
+                                double theta, double delta, double sigma, double rel_target, int max_applications,
+                                int degree, double* scal_dev, int* flag_dev, void* stream);
+HF_API int hf_coarse_destroy(hf_coarse* c);
 /* Jacobi-PCG / Lanczos range estimate with device-side scalars
  * (estimate_eigenvalue_range, multigrid.py:112-166): no host round trip per
  * iteration.  scal_dev[4]: [0] rz = r.z (set by hf_jacobi_dot before

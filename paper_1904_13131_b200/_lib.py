@@ -82,6 +82,9 @@ _SIGS = {
     "hf_jacobi_dot": (I, [P, LL, P, P, P, P, P]),
     "hf_axpby": (I, [LL, D, P, D, P, P]),
     "hf_lanczos_init": (I, [P, P, P]),
+    "hf_coarse_create": (I, [LL, LL, P, P, P, P, ct.POINTER(P)]),
+    "hf_coarse_cheb_solve": (I, [P, P, P, P, P, D, D, D, D, I, I, P, P, P]),
+    "hf_coarse_destroy": (I, [P]),
     "hf_lanczos_step": (I, [P, LL, P, P, P, P, P, P, P, P, P]),
     "hf_fill_masked_f32": (I, [LL, P, P, P, D, P]),
     "hf_cheb_step_f32": (I, [LL, P, P, P, P, P, I, D, D, D, I, P, P, P, P]),

@@ -13,6 +13,7 @@
 #include "../../include/hf.h"
 #include "hf_dispatch.h"
 #include "hf_vec.cuh"
+#include "hf_coarse.cuh"
 
 using namespace hf;
 
@@ -128,6 +129,17 @@ struct hf_transfer {
   double* d_rw[3] = {nullptr, nullptr, nullptr};
   double* d_tmp[2] = {nullptr, nullptr};
   long long tmp_len = 0;
+};
+
+struct hf_coarse {
+  int n = 0;
+  long long nnz = 0;
+  int grid = 1;
+  size_t smem = 0;
+  unsigned char* blob = nullptr;
+  long long* boff = nullptr;
+  double* xb = nullptr;
+  double* partials = nullptr;
 };
 
 struct hf_ws {
@@ -1087,6 +1099,126 @@ HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, cons
   if (!w || !z || !r || !inv_d || !out_dev) return fail(HF_ERR_ARG, "null argument");
   k_jacobi_dot<<<red_blocks(n), RED_THREADS, 0, S(stream)>>>(n, z, r, inv_d, w->d_partials, w->d_counter, out_dev);
   HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_coarse_create(long long n, long long nnz, const int* rowptr_dev, const int* col_dev,
+                            const double* val_dev, void* stream, hf_coarse** out) {
+  if (!out || n <= 0 || nnz < 0 || !rowptr_dev || (nnz > 0 && (!col_dev || !val_dev)))
+    return fail(HF_ERR_ARG, "bad coarse matrix");
+  if (n >= (1ll << 31) || nnz >= (1ll << 31)) return fail(HF_ERR_UNSUPPORTED, "coarse matrix too large");
+  cudaStream_t s = S(stream);
+  std::vector<int> rp(n + 1), cl(nnz);
+  std::vector<double> va(nnz);
+  HF_CUDA(cudaMemcpyAsync(rp.data(), rowptr_dev, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, s));
+  if (nnz > 0) {
+    HF_CUDA(cudaMemcpyAsync(cl.data(), col_dev, sizeof(int) * nnz, cudaMemcpyDeviceToHost, s));
+    HF_CUDA(cudaMemcpyAsync(va.data(), val_dev, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s));
+  }
+  HF_CUDA(cudaStreamSynchronize(s));
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // one CTA per SM (the grid barrier costs the same ~1.2 us from 35 to 148
+  // CTAs on B200, tools/probes/gridsync_probe.cu), fewer for tiny levels
+  const int grid = (int)std::max(1ll, std::min<long long>(nsm, (n + 7) / 8));
+  const int rows_per = (int)((n + grid - 1) / grid);
+  std::vector<unsigned char> blob;
+  std::vector<long long> boff(grid);
+  size_t smem = 0;
+  for (int c = 0; c < grid; ++c) {
+    const int r0 = std::min<long long>(n, (long long)c * rows_per), r1 = std::min<long long>(n, (long long)r0 + rows_per);
+    const int rows = r1 - r0;
+    const int k0 = rp[r0], k1 = rp[r1], nz = k1 - k0;
+    std::vector<int> u(cl.begin() + k0, cl.begin() + k1);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    if (u.size() > 65535) return fail(HF_ERR_UNSUPPORTED, "coarse CTA block touches too many columns");
+    const size_t body = coarse_align16(8ull * nz) + coarse_align16(4ull * u.size()) +
+                        coarse_align16(4ull * (rows + 1)) + coarse_align16(2ull * nz);
+    smem = std::max<size_t>(smem, body + 8 * (u.size() + 3 * (size_t)rows));
+    const size_t base = blob.size();
+    boff[c] = (long long)base;
+    blob.resize(base + 16 + body, 0);
+    CoarseBlock h = {r0, rows, (int)u.size(), nz};
+    std::memcpy(blob.data() + base, &h, sizeof(h));
+    unsigned char* p = blob.data() + base + 16;
+    std::memcpy(p, va.data() + k0, 8ull * nz);
+    p += coarse_align16(8ull * nz);
+    std::memcpy(p, u.data(), 4ull * u.size());
+    p += coarse_align16(4ull * u.size());
+    int* lr = reinterpret_cast<int*>(p);
+    for (int l = 0; l <= rows; ++l) lr[l] = rp[r0 + l] - k0;
+    p += coarse_align16(4ull * (rows + 1));
+    unsigned short* lc = reinterpret_cast<unsigned short*>(p);
+    for (int k = 0; k < nz; ++k)
+      lc[k] = (unsigned short)(std::lower_bound(u.begin(), u.end(), cl[k0 + k]) - u.begin());
+  }
+  if (smem > 200 * 1024) return fail(HF_ERR_UNSUPPORTED, "coarse level too large for the one-kernel solve");
+  HF_CUDA(cudaFuncSetAttribute(k_coarse_cheb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_cheb, COARSE_THREADS, smem));
+  if (per_sm < 1) return fail(HF_ERR_UNSUPPORTED, "coarse kernel cannot be resident");
+  hf_coarse* c = new hf_coarse();
+  c->n = (int)n;
+  c->nnz = nnz;
+  c->grid = grid;
+  c->smem = smem;
+  HF_CUDA(cudaMalloc((void**)&c->blob, blob.size()));
+  HF_CUDA(cudaMalloc((void**)&c->boff, sizeof(long long) * grid));
+  HF_CUDA(cudaMalloc((void**)&c->xb, sizeof(double) * n));
+  HF_CUDA(cudaMalloc((void**)&c->partials, sizeof(double) * grid));
+  HF_CUDA(cudaMemcpyAsync(c->blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+  HF_CUDA(cudaMemcpyAsync(c->boff, boff.data(), sizeof(long long) * grid, cudaMemcpyHostToDevice, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  *out = c;
+  return HF_OK;
+}
+
+HF_API int hf_coarse_destroy(hf_coarse* c) {
+  if (!c) return HF_OK;
+  cudaFree(c->blob);
+  cudaFree(c->boff);
+  cudaFree(c->xb);
+  cudaFree(c->partials);
+  delete c;
+  return HF_OK;
+}
+
+HF_API int hf_coarse_cheb_solve(hf_coarse* c, const double* b, double* x, double* d, const double* inv_d,
+                                double theta, double delta, double sigma, double rel_target, int max_applications,
+                                int degree, double* scal_dev, int* flag_dev, void* stream) {
+  if (!c || !b || !x || !d || !inv_d || !scal_dev || !flag_dev || degree < 1)
+    return fail(HF_ERR_ARG, "null argument or degree < 1");
+  CoarseArgs a;
+  a.n = c->n;
+  a.blob = c->blob;
+  a.boff = c->boff;
+  a.b = b;
+  a.inv_d = inv_d;
+  a.x = x;
+  a.xb = c->xb;
+  a.d = d;
+  a.partials = c->partials;
+  a.scal = scal_dev;
+  a.flag = flag_dev;
+  a.theta = theta;
+  a.delta = delta;
+  a.sigma = sigma;
+  a.rel_target = rel_target;
+  a.max_applications = max_applications;
+  a.degree = degree;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)c->grid);
+  cfg.blockDim = dim3(COARSE_THREADS);
+  cfg.dynamicSmemBytes = c->smem;
+  cfg.stream = S(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HF_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_cheb, a));
   return HF_OK;
 }
 

@@ -28,10 +28,10 @@ import scipy.linalg
 import torch
 
 from . import device as dv
-from ._lib import check, lib
+from ._lib import HF_ERR_UNSUPPORTED, HfError, check, lib
 from .fespace import interpolation_matrix_1d
 from .material import NonPositiveJacobian
-from .operators import MatrixFreeTangent, Problem
+from .operators import AssembledTangent, MatrixFreeTangent, Problem
 
 log = logging.getLogger(__name__)
 
@@ -267,6 +267,42 @@ def chebyshev_apply(apply_fn, inv_diagonal, lam_max: float, b, x, settings: Cheb
     return dv.like_input(xd, x)
 
 
+def _coarse_kernel_enabled(problem: Problem) -> bool:
+    """The one-kernel coarse solve needs the assembled level matrix (element
+    matrices are instantiated for 3D Q1-Q2 and 2D Q1-Q4) and a small level.
+    HF_COARSE=launches keeps the per-application graph launches."""
+    import os
+
+    if os.environ.get("HF_COARSE", "kernel") == "launches":
+        return False
+    n1 = problem.degree + 1
+    ok = (problem.dim == 3 and n1 <= 3) or (problem.dim == 2 and n1 <= 5)
+    return ok and problem.n_dofs <= 200_000
+
+
+class _CoarseMatrix:
+    """Assembled coarsest-level tangent (AssembledTangent's CSR: constrained rows
+    and columns cleared, unit diagonal) handed to hf_coarse_create."""
+
+    def __init__(self, problem: Problem, u_level):
+        m = AssembledTangent(problem, u_level).matrix
+        crow = m.crow_indices().to(torch.int32)
+        col = m.col_indices().to(torch.int32)
+        val = m.values().contiguous()
+        h = ct.c_void_p()
+        check(lib().hf_coarse_create(problem.n_dofs, val.numel(), dv.ptr(crow), dv.ptr(col), dv.ptr(val),
+                                     dv.stream(), ct.byref(h)))
+        self._h = h
+        self.nnz = val.numel()
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().hf_coarse_destroy(self._h)
+        except Exception:
+            pass
+
+
 class LevelOperator:
     """Tangent of one level plus its smoother data (multigrid.py:208-252)."""
 
@@ -303,6 +339,13 @@ class LevelOperator:
         elif precision != "fp64":
             raise ValueError(f"unknown precision {precision!r}")
         self._cap_warned = False
+        self.coarse = None
+        if is_coarsest and precision == "fp64" and _coarse_kernel_enabled(problem):
+            try:
+                self.coarse = _CoarseMatrix(problem, u_level)
+            except HfError as err:  # level too large for the shared-memory blocks: per-application launches
+                if err.code != HF_ERR_UNSUPPORTED:
+                    raise
         n = problem.n_dofs
         # per-level V-cycle buffers
         self.b = torch.zeros(n, dtype=dtype, device="cuda")
@@ -345,6 +388,12 @@ def _coarse_solve_into(level: LevelOperator, b, x, rel_target=1e-3, max_applicat
     sigma = theta / delta
     n = b.numel()
     L = lib()
+    if level.coarse is not None and x.dtype == torch.float64:
+        # the whole iteration as one persistent kernel on the assembled level matrix
+        check(L.hf_coarse_cheb_solve(level.coarse._h, dv.ptr(b), dv.ptr(x), dv.ptr(level.d), dv.ptr(level.inv_diag),
+                                     theta, delta, sigma, rel_target, max_applications, s.degree,
+                                     dv.ptr(level.scal), dv.ptr(level.flag), dv.stream()))
+        return x
     ws = dv.Workspace.get().handle
     scal, flag, d, ax = level.scal, level.flag, level.d, level.ax
     f32 = x.dtype == torch.float32

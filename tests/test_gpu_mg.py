@@ -132,3 +132,75 @@ def test_newton_prescribed_golden():
     assert np.all(np.abs(recs[:, 4] - ref[:, 4]) <= 1)
     assert np.allclose(recs[:, 2], ref[:, 2], rtol=1e-3, atol=1e-11)
     assert rel(res.u.cpu().numpy(), g["u"]) < 1e-8
+
+
+def _coarse_reference(A, inv_d, b, lv, rel_target, max_applications=100):
+    """coarse_solve (multigrid.py:255-306) in extended precision (np.longdouble)
+    on the assembled level matrix: the yardstick for both fp64 paths."""
+    from paper_1904_13131_b200.multigrid import ChebyshevSettings
+
+    s = lv.coarse_settings(ChebyshevSettings())
+    ld = np.longdouble
+    theta = ld(0.5) * (ld(s.range_hi) + ld(s.range_lo)) * ld(lv.lam_max)
+    delta = ld(0.5) * (ld(s.range_hi) - ld(s.range_lo)) * ld(lv.lam_max)
+    sigma = theta / delta
+    A, inv_d, b = A.astype(ld), inv_d.astype(ld), b.astype(ld)
+    target = ld(rel_target) * np.sqrt(b @ b)
+    d = inv_d * b / theta
+    x = d.copy()
+    rho_old = 1 / sigma
+    for step in range(2, max_applications + 1):
+        ax = A @ x
+        if step % s.degree == 0 and np.sqrt((b - ax) @ (b - ax)) <= target:
+            return x.astype(np.float64), True
+        rho = 1 / (2 * sigma - rho_old)
+        d = rho * rho_old * d + 2 * rho / delta * (inv_d * (b - ax))
+        x = x + d
+        rho_old = rho
+    return x.astype(np.float64), False
+
+
+def test_coarse_kernel_matches_launches(case, monkeypatch):
+    """The one-kernel coarse solve (hf_coarse_cheb_solve on the assembled level
+    matrix) against the per-application launches on the matrix-free operator
+    and an extended-precision restatement of the same iteration.  The coarse
+    levels of these cases are ill-conditioned: a 99-application Chebyshev
+    iterate amplifies fp64 rounding (summation order of CSR vs matrix-free
+    applies) to ~1e-6, so the check is that the kernel is as close to the
+    extended-precision iterate as the launches are.  The stop/cap flag agrees,
+    b = 0 returns x = 0, and GMG-CG takes the same number of iterations."""
+    from paper_1904_13131_b200 import MatrixFreeTangent, build_gmg, cg
+    from paper_1904_13131_b200.multigrid import LevelOperator, coarse_solve, restrict_solution
+    from paper_1904_13131_b200.operators import AssembledTangent
+
+    g, probs, transfers, _ = case
+    u0 = restrict_solution(probs, g["ubar"])[0]
+    lv = {}
+    for mode in ("kernel", "launches"):
+        monkeypatch.setenv("HF_COARSE", mode)
+        lv[mode] = LevelOperator(probs[0], u0, str(g["strategy"]), seed=0, level=0, is_coarsest=True)
+    assert lv["kernel"].coarse is not None and lv["launches"].coarse is None
+    A = AssembledTangent(probs[0], u0).matrix.to_dense().cpu().numpy()
+    inv_d = lv["kernel"].inv_diag.cpu().numpy()
+    rng = np.random.default_rng(4)
+    for rel_target in (1e-3, 1e-9):
+        b = rng.standard_normal(probs[0].n_dofs)
+        b[probs[0].constraints.mask] = 0.0
+        xk = coarse_solve(lv["kernel"], b, rel_target=rel_target)
+        xl = coarse_solve(lv["launches"], b, rel_target=rel_target)
+        xr, converged = _coarse_reference(A, inv_d, b, lv["kernel"], rel_target)
+        ek, el = rel(xk, xr), rel(xl, xr)
+        assert ek < max(1e-11, 10 * el), (rel_target, ek, el)
+        assert ek < 1e-4
+        assert lv["kernel"].cap_reached() == lv["launches"].cap_reached() == (not converged)
+    z = coarse_solve(lv["kernel"], np.zeros(probs[0].n_dofs))
+    assert not np.any(z) and not lv["kernel"].cap_reached()
+    its = {}
+    for mode in ("kernel", "launches"):
+        monkeypatch.setenv("HF_COARSE", mode)
+        gmg = build_gmg(probs, g["ubar"], str(g["strategy"]), seed=0, transfers=transfers)
+        assert (gmg.levels[0].coarse is not None) == (mode == "kernel")
+        op = MatrixFreeTangent(probs[-1], g["ubar"], str(g["strategy"]))
+        its[mode] = cg(op, g["b"], rel_tol=1e-8, preconditioner=gmg)
+    assert abs(its["kernel"][1].iterations - its["launches"][1].iterations) <= 1
+    assert rel(its["kernel"][0], its["launches"][0]) < 1e-6
