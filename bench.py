@@ -362,7 +362,8 @@ def run_ours(args):
                          "peak_source": peak_kind, "algorithmic_bytes_per_launch": ab,
                          "kernel_ms": kern_ms, "kernel": KERNEL},
             "e2e": {"value": n_global / e2e_ms / 1e6, "unit": "GDoF/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "pipeline": op.host_info() if public is None and hasattr(op, "host_info") else None},
             "gpu_launches": launches * args.steps, "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_extra:
         line.update(_extras(args, hbm, prob, ubar, x, y, flush, nqp))

@@ -137,6 +137,16 @@ HF_API int hf_tangent_apply_tiles(hf_tangent* op, const double* x_dev, double* y
  * once the stream is synchronised.  Uses device staging vectors owned by the
  * tangent, so calls on one tangent must not run concurrently. */
 HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y_host, int chunks, void* stream);
+/* The pipeline runs one of four ways: captured as a CUDA graph or enqueued
+ * directly, each with the copy directions overlapping or with every D2H held
+ * back until the last H2D is done.  On first use per buffer pair all four are
+ * timed on this host and the fastest kept (hosts differ: on some, concurrent
+ * H2D + D2H is slower than back to back, or a graph with host-memory copy
+ * nodes launches slower than direct enqueues).  HF_E2E_ORDER=0..3 forces one.
+ * hf_tangent_host_info: the variant kept by the last calibration (0 graph +
+ * overlap, 1 graph + serial, 2 direct + overlap, 3 direct + serial, -1 none)
+ * and the four measured step times in us (us4[4], 0 if not measured). */
+HF_API int hf_tangent_host_info(const hf_tangent* op, int* variant, float* us4);
 /* page-lock / release caller-owned host memory (cudaHostRegister) */
 HF_API int hf_host_register(void* host_ptr, long long bytes);
 HF_API int hf_host_unregister(void* host_ptr);

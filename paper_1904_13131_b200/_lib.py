@@ -53,6 +53,7 @@ _SIGS = {
     "hf_tangent_apply_tiles": (I, [P, P, P, P, LL, LL, I, P]),
     "hf_tangent_apply_host": (I, [P, P, P, I, P]),
     "hf_host_register": (I, [P, LL]),
+    "hf_tangent_host_info": (I, [P, ct.POINTER(I), ct.POINTER(ct.c_float)]),
     "hf_host_unregister": (I, [P]),
     "hf_tangent_diagonal": (I, [P, P, P]),
     "hf_tangent_assemble_local": (I, [P, P, P]),

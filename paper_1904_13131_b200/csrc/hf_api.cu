@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -99,11 +100,15 @@ struct HostPipe {
     const void* x;
     void* y;
     int chunks;
-    cudaGraphExec_t exec;
+    cudaGraphExec_t exec;  // null: enqueue directly (variant 2 overlap / 3 serial)
     unsigned long long used;
+    int variant;
   } g[NG] = {};
   int ng = 0;
   unsigned long long clock = 0;
+  int last_order = -1;           // variant of the last calibration: 0 graph overlap, 1 graph serial,
+                                 // 2 direct overlap, 3 direct serial
+  float last_us[4] = {0, 0, 0, 0};  // their calibration times
 };
 
 struct hf_tangent {
@@ -555,7 +560,8 @@ HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, 
 // ---- host-to-host apply: slab pipeline captured once per buffer pair ----
 static void host_pipe_free(HostPipe* h) {
   if (!h) return;
-  for (int i = 0; i < h->ng; ++i) cudaGraphExecDestroy(h->g[i].exec);
+  for (int i = 0; i < h->ng; ++i)
+    if (h->g[i].exec) cudaGraphExecDestroy(h->g[i].exec);
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   if (h->cap) cudaStreamDestroy(h->cap);
   if (h->s_in) cudaStreamDestroy(h->s_in);
@@ -583,7 +589,7 @@ static bool page_locked(const void* p, long long bytes) {
 // the last axis slowest, so a slab touches a contiguous range of node planes,
 // i.e. a contiguous DoF range.  H2D of each slab's new planes runs on s_in,
 // fill + cell kernel on cap, D2H of the planes no later slab touches on s_out.
-static int host_pipe_enqueue(hf_tangent* op, HostPipe* h, const double* xh, double* yh, int chunks) {
+static int host_pipe_enqueue(hf_tangent* op, HostPipe* h, const double* xh, double* yh, int chunks, bool serial) {
   const hf_space* sp = op->sp;
   const int d = sp->dim, deg = sp->degree;
   const long long layer = d == 3 ? (long long)sp->lat.cells[0] * sp->lat.cells[1] : sp->lat.cells[0];
@@ -605,7 +611,7 @@ static int host_pipe_enqueue(hf_tangent* op, HostPipe* h, const double* xh, doub
     lo = z0 * deg;
     hi = (z1 + 1) * deg + 1;
   };
-  const size_t need = 2 * cuts.size() + 4;
+  const size_t need = 2 * cuts.size() + 6;
   while (h->ev.size() < need) {
     cudaEvent_t e;
     HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -616,19 +622,29 @@ static int host_pipe_enqueue(hf_tangent* op, HostPipe* h, const double* xh, doub
   HF_CUDA(cudaStreamWaitEvent(h->s_in, h->ev[ie], 0));
   HF_CUDA(cudaStreamWaitEvent(h->s_out, h->ev[ie], 0));
   ++ie;
-  long long copied = 0, filled = 0, sent = 0;
+  // H2D of every slab's new node planes, in slab order on s_in (one event each)
+  std::vector<size_t> in_ev(cuts.size(), 0);
+  long long copied = 0;
   for (size_t k = 0; k + 1 < cuts.size(); ++k) {
-    const long long t0 = cuts[k], t1 = cuts[k + 1];
     long long lo, hi;
-    planes(t0, t1, lo, hi);
+    planes(cuts[k], cuts[k + 1], lo, hi);
     if (hi > copied) {
       HF_CUDA(cudaMemcpyAsync(h->xd + copied * plane, xh + copied * plane, sizeof(double) * (hi - copied) * plane,
                               cudaMemcpyHostToDevice, h->s_in));
       copied = hi;
       HF_CUDA(cudaEventRecord(h->ev[ie], h->s_in));
-      HF_CUDA(cudaStreamWaitEvent(h->cap, h->ev[ie], 0));
-      ++ie;
+      in_ev[k] = ie++;
     }
+  }
+  // serial: no D2H while any H2D is in flight (on hosts where the two copy
+  // directions do not overlap, concurrent traffic is slower than back to back)
+  if (serial) HF_CUDA(cudaStreamWaitEvent(h->s_out, h->ev[ie - 1], 0));
+  long long filled = 0, sent = 0;
+  for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+    const long long t0 = cuts[k], t1 = cuts[k + 1];
+    long long lo, hi;
+    planes(t0, t1, lo, hi);
+    if (in_ev[k]) HF_CUDA(cudaStreamWaitEvent(h->cap, h->ev[in_ev[k]], 0));
     int mode = 0;
     if (hi > filled) {
       const long long off = filled * plane, cnt = (hi - filled) * plane;
@@ -660,6 +676,15 @@ static int host_pipe_enqueue(hf_tangent* op, HostPipe* h, const double* xh, doub
   ++ie;
   HF_CUDA(cudaEventRecord(h->ev[ie], h->s_out));
   HF_CUDA(cudaStreamWaitEvent(h->cap, h->ev[ie], 0));
+  return HF_OK;
+}
+
+HF_API int hf_tangent_host_info(const hf_tangent* op, int* variant, float* us4) {
+  if (!op) return fail(HF_ERR_ARG, "null tangent");
+  const HostPipe* h = op->host;
+  if (variant) *variant = h ? h->last_order : -1;
+  if (us4)
+    for (int v = 0; v < 4; ++v) us4[v] = h ? h->last_us[v] : 0.f;
   return HF_OK;
 }
 
@@ -698,35 +723,103 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
   HostPipe::Entry* hit = nullptr;
   for (int i = 0; i < h->ng; ++i)
     if (h->g[i].x == x_host && h->g[i].y == y_host && h->g[i].chunks == chunks) hit = &h->g[i];
+  // enqueue directly on `stream` (no graph): fork/join through the pipe's streams
+  auto direct = [&](bool serial) -> int {
+    cudaEvent_t fork;
+    HF_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    HF_CUDA(cudaEventRecord(fork, S(stream)));
+    HF_CUDA(cudaStreamWaitEvent(h->cap, fork, 0));
+    cudaEventDestroy(fork);
+    const int rc = host_pipe_enqueue(op, h, x_host, y_host, chunks, serial);
+    if (rc != HF_OK) return rc;
+    cudaEvent_t join;
+    HF_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    HF_CUDA(cudaEventRecord(join, h->cap));
+    HF_CUDA(cudaStreamWaitEvent(S(stream), join, 0));
+    cudaEventDestroy(join);
+    return HF_OK;
+  };
   if (!hit) {
-    cudaGraph_t graph;
-    HF_CUDA(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
-    const int rc = host_pipe_enqueue(op, h, x_host, y_host, chunks);
-    const cudaError_t ce = cudaStreamEndCapture(h->cap, &graph);
-    if (rc != HF_OK) {
-      if (ce == cudaSuccess) cudaGraphDestroy(graph);
-      return rc;
+    // Four ways to run the pipeline: captured as a graph or enqueued directly,
+    // each with the copy directions overlapping or with every D2H held back
+    // until the last H2D is done.  On first use per buffer pair all four are
+    // timed on this host and the fastest is kept (hosts differ: on some,
+    // concurrent H2D + D2H is slower than back to back, and graph launches with
+    // host-memory copy nodes cost more than direct enqueues).
+    // HF_E2E_ORDER=0..3 forces one.
+    const char* env = std::getenv("HF_E2E_ORDER");
+    const int force = env ? std::atoi(env) : -1;
+    cudaGraphExec_t cand[2] = {nullptr, nullptr};
+    for (int v = 0; v < 2; ++v) {
+      if (force >= 0 && v != force) continue;
+      cudaGraph_t graph;
+      HF_CUDA(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+      const int rc = host_pipe_enqueue(op, h, x_host, y_host, chunks, v == 1);
+      const cudaError_t ce = cudaStreamEndCapture(h->cap, &graph);
+      if (rc != HF_OK) {
+        if (ce == cudaSuccess) cudaGraphDestroy(graph);
+        if (cand[0]) cudaGraphExecDestroy(cand[0]);
+        return rc;
+      }
+      HF_CUDA(ce);
+      const cudaError_t ie = cudaGraphInstantiate(&cand[v], graph, 0);
+      cudaGraphDestroy(graph);
+      HF_CUDA(ie);
     }
-    HF_CUDA(ce);
-    cudaGraphExec_t exec;
-    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    HF_CUDA(ie);
+    int keep = force >= 0 && force <= 3 ? force : -1;
+    if (keep < 0) {
+      float best = 1e30f;
+      for (int v = 0; v < 4; ++v) {
+        auto run = [&]() -> int {
+          if (v < 2) {
+            HF_CUDA(cudaGraphLaunch(cand[v], S(stream)));
+            return HF_OK;
+          }
+          return direct(v == 3);
+        };
+        int rc = HF_OK;
+        for (int w = 0; w < 2 && rc == HF_OK; ++w) rc = run();
+        if (rc != HF_OK) return rc;
+        HF_CUDA(cudaStreamSynchronize(S(stream)));
+        // host wall time of one synchronised step (enqueue cost included),
+        // best of 5: the host link is noisy
+        float us = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+          const auto t0 = std::chrono::steady_clock::now();
+          rc = run();
+          if (rc != HF_OK) return rc;
+          HF_CUDA(cudaStreamSynchronize(S(stream)));
+          us = std::min(us, std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - t0).count());
+        }
+        h->last_us[v] = us;
+        if (us < best) {
+          best = us;
+          keep = v;
+        }
+      }
+    }
+    for (int v = 0; v < 2; ++v)
+      if (cand[v] && v != keep) cudaGraphExecDestroy(cand[v]);
+    cudaGraphExec_t exec = keep < 2 ? cand[keep] : nullptr;
+    h->last_order = keep;
     int slot = h->ng;
     if (slot == HostPipe::NG) {  // evict the least recently used pipeline
       slot = 0;
       for (int i = 1; i < h->ng; ++i)
         if (h->g[i].used < h->g[slot].used) slot = i;
-      cudaGraphExecDestroy(h->g[slot].exec);
+      if (h->g[slot].exec) cudaGraphExecDestroy(h->g[slot].exec);
     } else {
       ++h->ng;
     }
-    h->g[slot] = {x_host, y_host, chunks, exec, 0};
+    h->g[slot] = {x_host, y_host, chunks, exec, 0, keep};
     hit = &h->g[slot];
   }
   hit->used = ++h->clock;
-  HF_CUDA(cudaGraphLaunch(hit->exec, S(stream)));
-  return HF_OK;
+  if (hit->exec) {
+    HF_CUDA(cudaGraphLaunch(hit->exec, S(stream)));
+    return HF_OK;
+  }
+  return direct(hit->variant == 3);
 }
 
 HF_API int hf_tangent_assemble_local(hf_tangent* op, double* vals_dev, void* stream) {

@@ -382,6 +382,15 @@ class MatrixFreeTangent:
         torch.cuda.current_stream().synchronize()
         return yh
 
+    def host_info(self) -> dict:
+        """How the host pipeline runs on this host (hf_tangent_host_info): the
+        variant kept and the calibration step times (us) of all four."""
+        v, us = ct.c_int(), (ct.c_float * 4)()
+        check(lib().hf_tangent_host_info(self._op, ct.byref(v), us))
+        names = ["graph+overlap", "graph+serial", "direct+overlap", "direct+serial"]
+        return {"variant": names[v.value] if v.value >= 0 else None,
+                "calibration_us": {names[i]: round(us[i], 1) for i in range(4)}}
+
     def __call__(self, x):
         return self.apply(x)
 
