@@ -250,6 +250,17 @@ HF_API int hf_coarse_cheb_solve(hf_coarse* c, const double* b, double* x, double
                                 double theta, double delta, double sigma, double rel_target, int max_applications,
                                 int degree, double* scal_dev, int* flag_dev, void* stream);
 HF_API int hf_coarse_destroy(hf_coarse* c);
+/* The same from a level directly: the sparsity pattern of the space's cell
+ * DoF map with the constraint mask applied (constrained rows and columns
+ * cleared, unit diagonal; operators.py:471-490) is built once on the host;
+ * hf_coarse_update then (asynchronously) refreshes the values from the element
+ * matrices of an fp64 tensor4 tangent on that space, each value the sum of its
+ * element entries in a fixed order -- no host work per Newton iteration.
+ * hf_coarse_clone gives an independent handle (own values and buffers) with
+ * the same pattern.  3D Q1-Q2 and 2D Q1-Q4. */
+HF_API int hf_coarse_create_space(const hf_space* sp, void* stream, hf_coarse** out);
+HF_API int hf_coarse_update(hf_coarse* c, hf_tangent* op, void* stream);
+HF_API int hf_coarse_clone(const hf_coarse* src, void* stream, hf_coarse** out);
 /* Jacobi-PCG / Lanczos range estimate with device-side scalars
  * (estimate_eigenvalue_range, multigrid.py:112-166): no host round trip per
  * iteration.  scal_dev[4]: [0] rz = r.z (set by hf_jacobi_dot before

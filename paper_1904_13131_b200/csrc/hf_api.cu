@@ -142,9 +142,17 @@ struct hf_coarse {
   int grid = 1;
   size_t smem = 0;
   unsigned char* blob = nullptr;
+  size_t blob_bytes = 0;
   long long* boff = nullptr;
   double* xb = nullptr;
   double* partials = nullptr;
+  // value refresh from element matrices (hf_coarse_create_space / hf_coarse_update)
+  const hf_space* sp = nullptr;
+  int nupd = 0;                 // CSR slots with element contributions
+  int* cptr = nullptr;          // [nupd + 1] contributions of slot u
+  int* cidx = nullptr;          // element-matrix entry indices, ascending per slot
+  long long* uoff = nullptr;    // blob byte offset of slot u's value
+  double* elem = nullptr;       // element matrices scratch
 };
 
 struct hf_ws {
@@ -1195,6 +1203,76 @@ HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, cons
   return HF_OK;
 }
 
+// Pack a host CSR into per-CTA shared-memory blocks (CoarseBlock) and upload;
+// slot_off[k] receives the blob byte offset of CSR value k.
+static int coarse_build(long long n, long long nnz, const std::vector<int>& rp, const std::vector<int>& cl,
+                        const std::vector<double>& va, cudaStream_t s, hf_coarse** out,
+                        std::vector<long long>* slot_off) {
+  if (n >= (1ll << 31) || nnz >= (1ll << 31)) return fail(HF_ERR_UNSUPPORTED, "coarse matrix too large");
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // one CTA per SM (the grid barrier costs the same ~1.2 us from 35 to 148
+  // CTAs on B200, tools/probes/gridsync_probe.cu), fewer for tiny levels
+  const int grid = (int)std::max(1ll, std::min<long long>(nsm, (n + 7) / 8));
+  const int rows_per = (int)((n + grid - 1) / grid);
+  std::vector<unsigned char> blob;
+  std::vector<long long> boff(grid);
+  if (slot_off) slot_off->assign(nnz, 0);
+  std::vector<int> pos(n, -1);
+  size_t smem = 0;
+  for (int c = 0; c < grid; ++c) {
+    const int r0 = std::min<long long>(n, (long long)c * rows_per), r1 = std::min<long long>(n, (long long)r0 + rows_per);
+    const int rows = r1 - r0;
+    const int k0 = rp[r0], k1 = rp[r1], nz = k1 - k0;
+    std::vector<int> u(cl.begin() + k0, cl.begin() + k1);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    if (u.size() > 65535) return fail(HF_ERR_UNSUPPORTED, "coarse CTA block touches too many columns");
+    for (size_t q = 0; q < u.size(); ++q) pos[u[q]] = (int)q;
+    const size_t body = coarse_align16(8ull * nz) + coarse_align16(4ull * u.size()) +
+                        coarse_align16(4ull * (rows + 1)) + coarse_align16(2ull * nz);
+    smem = std::max<size_t>(smem, body + 8 * (u.size() + 3 * (size_t)rows));
+    const size_t base = blob.size();
+    boff[c] = (long long)base;
+    blob.resize(base + 16 + body, 0);
+    CoarseBlock h = {r0, rows, (int)u.size(), nz};
+    std::memcpy(blob.data() + base, &h, sizeof(h));
+    unsigned char* p = blob.data() + base + 16;
+    std::memcpy(p, va.data() + k0, 8ull * nz);
+    if (slot_off)
+      for (int k = 0; k < nz; ++k) (*slot_off)[k0 + k] = (long long)(base + 16 + 8ull * k);
+    p += coarse_align16(8ull * nz);
+    std::memcpy(p, u.data(), 4ull * u.size());
+    p += coarse_align16(4ull * u.size());
+    int* lr = reinterpret_cast<int*>(p);
+    for (int l = 0; l <= rows; ++l) lr[l] = rp[r0 + l] - k0;
+    p += coarse_align16(4ull * (rows + 1));
+    unsigned short* lc = reinterpret_cast<unsigned short*>(p);
+    for (int k = 0; k < nz; ++k) lc[k] = (unsigned short)pos[cl[k0 + k]];
+  }
+  if (smem > 200 * 1024) return fail(HF_ERR_UNSUPPORTED, "coarse level too large for the one-kernel solve");
+  HF_CUDA(cudaFuncSetAttribute(k_coarse_cheb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_cheb, COARSE_THREADS, smem));
+  if (per_sm < 1) return fail(HF_ERR_UNSUPPORTED, "coarse kernel cannot be resident");
+  hf_coarse* c = new hf_coarse();
+  c->n = (int)n;
+  c->nnz = nnz;
+  c->grid = grid;
+  c->smem = smem;
+  c->blob_bytes = blob.size();
+  HF_CUDA(cudaMalloc((void**)&c->blob, blob.size()));
+  HF_CUDA(cudaMalloc((void**)&c->boff, sizeof(long long) * grid));
+  HF_CUDA(cudaMalloc((void**)&c->xb, sizeof(double) * n));
+  HF_CUDA(cudaMalloc((void**)&c->partials, sizeof(double) * grid));
+  HF_CUDA(cudaMemcpyAsync(c->blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
+  HF_CUDA(cudaMemcpyAsync(c->boff, boff.data(), sizeof(long long) * grid, cudaMemcpyHostToDevice, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  *out = c;
+  return HF_OK;
+}
+
 HF_API int hf_coarse_create(long long n, long long nnz, const int* rowptr_dev, const int* col_dev,
                             const double* val_dev, void* stream, hf_coarse** out) {
   if (!out || n <= 0 || nnz < 0 || !rowptr_dev || (nnz > 0 && (!col_dev || !val_dev)))
@@ -1209,61 +1287,151 @@ HF_API int hf_coarse_create(long long n, long long nnz, const int* rowptr_dev, c
     HF_CUDA(cudaMemcpyAsync(va.data(), val_dev, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s));
   }
   HF_CUDA(cudaStreamSynchronize(s));
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // one CTA per SM (the grid barrier costs the same ~1.2 us from 35 to 148
-  // CTAs on B200, tools/probes/gridsync_probe.cu), fewer for tiny levels
-  const int grid = (int)std::max(1ll, std::min<long long>(nsm, (n + 7) / 8));
-  const int rows_per = (int)((n + grid - 1) / grid);
-  std::vector<unsigned char> blob;
-  std::vector<long long> boff(grid);
-  size_t smem = 0;
-  for (int c = 0; c < grid; ++c) {
-    const int r0 = std::min<long long>(n, (long long)c * rows_per), r1 = std::min<long long>(n, (long long)r0 + rows_per);
-    const int rows = r1 - r0;
-    const int k0 = rp[r0], k1 = rp[r1], nz = k1 - k0;
-    std::vector<int> u(cl.begin() + k0, cl.begin() + k1);
-    std::sort(u.begin(), u.end());
-    u.erase(std::unique(u.begin(), u.end()), u.end());
-    if (u.size() > 65535) return fail(HF_ERR_UNSUPPORTED, "coarse CTA block touches too many columns");
-    const size_t body = coarse_align16(8ull * nz) + coarse_align16(4ull * u.size()) +
-                        coarse_align16(4ull * (rows + 1)) + coarse_align16(2ull * nz);
-    smem = std::max<size_t>(smem, body + 8 * (u.size() + 3 * (size_t)rows));
-    const size_t base = blob.size();
-    boff[c] = (long long)base;
-    blob.resize(base + 16 + body, 0);
-    CoarseBlock h = {r0, rows, (int)u.size(), nz};
-    std::memcpy(blob.data() + base, &h, sizeof(h));
-    unsigned char* p = blob.data() + base + 16;
-    std::memcpy(p, va.data() + k0, 8ull * nz);
-    p += coarse_align16(8ull * nz);
-    std::memcpy(p, u.data(), 4ull * u.size());
-    p += coarse_align16(4ull * u.size());
-    int* lr = reinterpret_cast<int*>(p);
-    for (int l = 0; l <= rows; ++l) lr[l] = rp[r0 + l] - k0;
-    p += coarse_align16(4ull * (rows + 1));
-    unsigned short* lc = reinterpret_cast<unsigned short*>(p);
-    for (int k = 0; k < nz; ++k)
-      lc[k] = (unsigned short)(std::lower_bound(u.begin(), u.end(), cl[k0 + k]) - u.begin());
+  return coarse_build(n, nnz, rp, cl, va, s, out, nullptr);
+}
+
+// The level's sparsity pattern from the cell DoF map and the constraint mask
+// (AssembledTangent, operators.py:471-490: constrained rows/columns cleared,
+// unit diagonal), built once on the host; values come later from element
+// matrices (hf_coarse_update), summed per CSR slot in ascending entry order.
+HF_API int hf_coarse_create_space(const hf_space* sp, void* stream, hf_coarse** out) {
+  if (!sp || !out) return fail(HF_ERR_ARG, "null argument");
+  if ((sp->dim == 3 && sp->n1 > 3) || (sp->dim == 2 && sp->n1 > 5))
+    return fail(HF_ERR_UNSUPPORTED, "element matrices are instantiated for 3D Q1-Q2 and 2D Q1-Q4");
+  cudaStream_t s = S(stream);
+  const long long nel = sp->lat.n_el, n = sp->n_dofs;
+  int nloc = 1;
+  for (int a = 0; a < sp->dim; ++a) nloc *= sp->n1;
+  const int nld = nloc * sp->dim;
+  if (n >= (1ll << 31) || nel * nld * nld >= (1ll << 31)) return fail(HF_ERR_UNSUPPORTED, "coarse level too large");
+  long long* d_dofs = nullptr;
+  HF_CUDA(cudaMalloc((void**)&d_dofs, sizeof(long long) * std::max(1ll, nel * nld)));
+  std::vector<long long> dofs(nel * nld);
+  std::vector<unsigned char> mask(n);
+  cudaError_t e = launch_cell_dofs(sp->lat, sp->dim, sp->degree, d_dofs, s);
+  if (e == cudaSuccess && nel > 0)
+    e = cudaMemcpyAsync(dofs.data(), d_dofs, sizeof(long long) * nel * nld, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(mask.data(), sp->d_mask, n, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d_dofs);
+  HF_CUDA(e);
+  struct Ent {
+    int r, c, k;  // k = element-matrix entry, -1 = unit diagonal of a constrained row
+  };
+  std::vector<Ent> ent;
+  ent.reserve((size_t)nel * nld * nld);
+  for (long long el = 0; el < nel; ++el)
+    for (int i = 0; i < nld; ++i) {
+      const int r = (int)dofs[el * nld + i];
+      if (mask[r]) continue;
+      for (int j = 0; j < nld; ++j) {
+        const int c = (int)dofs[el * nld + j];
+        if (!mask[c]) ent.push_back({r, c, (int)((el * nld + i) * nld + j)});
+      }
+    }
+  for (long long r = 0; r < n; ++r)
+    if (mask[r]) ent.push_back({(int)r, (int)r, -1});
+  std::sort(ent.begin(), ent.end(), [](const Ent& a, const Ent& b) {
+    return a.r != b.r ? a.r < b.r : (a.c != b.c ? a.c < b.c : a.k < b.k);
+  });
+  std::vector<int> rp(n + 1, 0), cl, cptr(1, 0), cidx;
+  std::vector<double> va;
+  std::vector<int> slot_of_upd;  // CSR slot of update u
+  for (size_t q = 0; q < ent.size();) {
+    size_t q1 = q;
+    while (q1 < ent.size() && ent[q1].r == ent[q].r && ent[q1].c == ent[q].c) ++q1;
+    const int slot = (int)cl.size();
+    cl.push_back(ent[q].c);
+    rp[ent[q].r + 1]++;
+    if (ent[q].k < 0) {
+      va.push_back(1.0);
+    } else {
+      va.push_back(0.0);
+      for (size_t t = q; t < q1; ++t) cidx.push_back(ent[t].k);
+      cptr.push_back((int)cidx.size());
+      slot_of_upd.push_back(slot);
+    }
+    q = q1;
   }
-  if (smem > 200 * 1024) return fail(HF_ERR_UNSUPPORTED, "coarse level too large for the one-kernel solve");
-  HF_CUDA(cudaFuncSetAttribute(k_coarse_cheb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_cheb, COARSE_THREADS, smem));
-  if (per_sm < 1) return fail(HF_ERR_UNSUPPORTED, "coarse kernel cannot be resident");
-  hf_coarse* c = new hf_coarse();
-  c->n = (int)n;
-  c->nnz = nnz;
-  c->grid = grid;
-  c->smem = smem;
-  HF_CUDA(cudaMalloc((void**)&c->blob, blob.size()));
-  HF_CUDA(cudaMalloc((void**)&c->boff, sizeof(long long) * grid));
-  HF_CUDA(cudaMalloc((void**)&c->xb, sizeof(double) * n));
-  HF_CUDA(cudaMalloc((void**)&c->partials, sizeof(double) * grid));
-  HF_CUDA(cudaMemcpyAsync(c->blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
-  HF_CUDA(cudaMemcpyAsync(c->boff, boff.data(), sizeof(long long) * grid, cudaMemcpyHostToDevice, s));
+  for (long long r = 0; r < n; ++r) rp[r + 1] += rp[r];
+  std::vector<long long> slot_off;
+  const int rc = coarse_build(n, (long long)cl.size(), rp, cl, va, s, out, &slot_off);
+  if (rc != HF_OK) return rc;
+  hf_coarse* c = *out;
+  c->sp = sp;
+  c->nupd = (int)slot_of_upd.size();
+  std::vector<long long> uoff(c->nupd);
+  for (int u = 0; u < c->nupd; ++u) uoff[u] = slot_off[slot_of_upd[u]];
+  HF_CUDA(cudaMalloc((void**)&c->cptr, sizeof(int) * (c->nupd + 1)));
+  HF_CUDA(cudaMalloc((void**)&c->cidx, sizeof(int) * std::max<size_t>(1, cidx.size())));
+  HF_CUDA(cudaMalloc((void**)&c->uoff, sizeof(long long) * std::max(1, c->nupd)));
+  HF_CUDA(cudaMalloc((void**)&c->elem, sizeof(double) * std::max(1ll, nel * nld * nld)));
+  HF_CUDA(cudaMemcpyAsync(c->cptr, cptr.data(), sizeof(int) * (c->nupd + 1), cudaMemcpyHostToDevice, s));
+  if (!cidx.empty())
+    HF_CUDA(cudaMemcpyAsync(c->cidx, cidx.data(), sizeof(int) * cidx.size(), cudaMemcpyHostToDevice, s));
+  if (c->nupd) HF_CUDA(cudaMemcpyAsync(c->uoff, uoff.data(), sizeof(long long) * c->nupd, cudaMemcpyHostToDevice, s));
   HF_CUDA(cudaStreamSynchronize(s));
+  return HF_OK;
+}
+
+// Refresh the values from the element matrices of a tensor4 fp64 tangent on
+// the same space (asynchronous; the sparsity pattern is unchanged).
+HF_API int hf_coarse_update(hf_coarse* c, hf_tangent* op, void* stream) {
+  if (!c || !op) return fail(HF_ERR_ARG, "null argument");
+  if (!c->sp || op->sp != c->sp) return fail(HF_ERR_ARG, "coarse handle was not created from this tangent's space");
+  if (op->strategy != HF_TENSOR4 || op->fp32) return fail(HF_ERR_ARG, "element matrices need an fp64 tensor4 tangent");
+  cudaStream_t s = S(stream);
+  CellArgs a = base_args(op->sp);
+  a.cache = op->d_cache;
+  HF_CUDA(launch_assemble(op->sp->dim, op->sp->n1, a, c->elem, s));
+  if (c->nupd) {
+    k_coarse_values<<<(unsigned)((c->nupd + 255) / 256), 256, 0, s>>>(c->nupd, c->cptr, c->cidx, c->elem, c->blob,
+                                                                      c->uoff);
+    HF_CUDA(cudaGetLastError());
+  }
+  return HF_OK;
+}
+
+// an independent handle with the same pattern (own values and iterate buffers)
+HF_API int hf_coarse_clone(const hf_coarse* src, void* stream, hf_coarse** out) {
+  if (!src || !out) return fail(HF_ERR_ARG, "null argument");
+  cudaStream_t s = S(stream);
+  hf_coarse* c = new hf_coarse(*src);
+  c->blob = nullptr;
+  c->boff = nullptr;
+  c->xb = nullptr;
+  c->partials = nullptr;
+  c->cptr = nullptr;
+  c->cidx = nullptr;
+  c->uoff = nullptr;
+  c->elem = nullptr;
+  auto dup = [&](void** dst, const void* from, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 8));
+    if (e == cudaSuccess && from && bytes) e = cudaMemcpyAsync(*dst, from, bytes, cudaMemcpyDeviceToDevice, s);
+    return e;
+  };
+  int nloc = 1, nld = 0;
+  if (src->sp) {
+    for (int a = 0; a < src->sp->dim; ++a) nloc *= src->sp->n1;
+    nld = nloc * src->sp->dim;
+  }
+  const long long nel = src->sp ? src->sp->lat.n_el : 0;
+  long long ncidx = 0;
+  if (src->nupd) HF_CUDA(cudaMemcpy(&ncidx, src->cptr + src->nupd, sizeof(int), cudaMemcpyDeviceToHost));
+  ncidx = (int)ncidx;
+  cudaError_t e = dup((void**)&c->blob, src->blob, src->blob_bytes);
+  if (e == cudaSuccess) e = dup((void**)&c->boff, src->boff, sizeof(long long) * src->grid);
+  if (e == cudaSuccess) e = dup((void**)&c->xb, nullptr, sizeof(double) * src->n);
+  if (e == cudaSuccess) e = dup((void**)&c->partials, nullptr, sizeof(double) * src->grid);
+  if (e == cudaSuccess && src->cptr) e = dup((void**)&c->cptr, src->cptr, sizeof(int) * (src->nupd + 1));
+  if (e == cudaSuccess && src->cidx) e = dup((void**)&c->cidx, src->cidx, sizeof(int) * ncidx);
+  if (e == cudaSuccess && src->uoff) e = dup((void**)&c->uoff, src->uoff, sizeof(long long) * src->nupd);
+  if (e == cudaSuccess && src->elem) e = dup((void**)&c->elem, nullptr, sizeof(double) * nel * nld * nld);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    hf_coarse_destroy(c);
+    return fail(HF_ERR_CUDA, std::string("hf_coarse_clone: ") + cudaGetErrorString(e));
+  }
   *out = c;
   return HF_OK;
 }
@@ -1274,6 +1442,10 @@ HF_API int hf_coarse_destroy(hf_coarse* c) {
   cudaFree(c->boff);
   cudaFree(c->xb);
   cudaFree(c->partials);
+  cudaFree(c->cptr);
+  cudaFree(c->cidx);
+  cudaFree(c->uoff);
+  cudaFree(c->elem);
   delete c;
   return HF_OK;
 }

@@ -191,4 +191,14 @@ __global__ void __launch_bounds__(COARSE_THREADS) k_coarse_cheb(const CoarseArgs
   }
 }
 
+// blob value of update slot u = sum of its element-matrix entries (ascending)
+__global__ void k_coarse_values(int nupd, const int* __restrict__ cptr, const int* __restrict__ cidx,
+                                const double* __restrict__ elem, unsigned char* blob, const long long* __restrict__ uoff) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= nupd) return;
+  double v = 0.0;
+  for (int k = cptr[u]; k < cptr[u + 1]; ++k) v += elem[cidx[k]];
+  *reinterpret_cast<double*>(blob + uoff[u]) = v;
+}
+
 }  // namespace hf

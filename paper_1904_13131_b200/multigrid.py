@@ -280,20 +280,11 @@ def _coarse_kernel_enabled(problem: Problem) -> bool:
     return ok and problem.n_dofs <= 200_000
 
 
-class _CoarseMatrix:
-    """Assembled coarsest-level tangent (AssembledTangent's CSR: constrained rows
-    and columns cleared, unit diagonal) handed to hf_coarse_create."""
+class _CoarseHandle:
+    """Owns one hf_coarse handle."""
 
-    def __init__(self, problem: Problem, u_level):
-        m = AssembledTangent(problem, u_level).matrix
-        crow = m.crow_indices().to(torch.int32)
-        col = m.col_indices().to(torch.int32)
-        val = m.values().contiguous()
-        h = ct.c_void_p()
-        check(lib().hf_coarse_create(problem.n_dofs, val.numel(), dv.ptr(crow), dv.ptr(col), dv.ptr(val),
-                                     dv.stream(), ct.byref(h)))
+    def __init__(self, h):
         self._h = h
-        self.nnz = val.numel()
 
     def __del__(self):
         try:
@@ -301,6 +292,31 @@ class _CoarseMatrix:
                 lib().hf_coarse_destroy(self._h)
         except Exception:
             pass
+
+
+class _CoarseMatrix:
+    """Assembled coarsest-level tangent for the one-kernel coarse solve.  The
+    sparsity pattern (cell DoFs + constraint mask) is built once per problem
+    and mask (hf_coarse_create_space, cached on the problem); each level
+    operator clones it and refreshes the values on the device from the
+    element matrices of a tensor4 tangent at the level's displacement
+    (hf_coarse_update) -- the same matrix AssembledTangent forms."""
+
+    def __init__(self, problem: Problem, u_level, op=None):
+        key = problem.constraints.mask.tobytes()
+        proto = getattr(problem, "_coarse_proto", None)
+        if proto is None or proto[0] != key:
+            h = ct.c_void_p()
+            check(lib().hf_coarse_create_space(problem._space, dv.stream(), ct.byref(h)))
+            proto = (key, _CoarseHandle(h))
+            problem._coarse_proto = proto
+        h = ct.c_void_p()
+        check(lib().hf_coarse_clone(proto[1]._h, dv.stream(), ct.byref(h)))
+        self._own = _CoarseHandle(h)
+        self._h = h
+        if op is None or op.strategy != "tensor4" or op.storage != "fp64":
+            op = MatrixFreeTangent(problem, u_level, "tensor4")  # NonPositiveJacobian propagates
+        check(lib().hf_coarse_update(h, op._op, dv.stream()))
 
 
 class LevelOperator:
@@ -342,7 +358,7 @@ class LevelOperator:
         self.coarse = None
         if is_coarsest and precision == "fp64" and _coarse_kernel_enabled(problem):
             try:
-                self.coarse = _CoarseMatrix(problem, u_level)
+                self.coarse = _CoarseMatrix(problem, u_level, self.op)
             except HfError as err:  # level too large for the shared-memory blocks: per-application launches
                 if err.code != HF_ERR_UNSUPPORTED:
                     raise
