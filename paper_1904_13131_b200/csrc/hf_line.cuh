@@ -262,9 +262,10 @@ HF_DEV void gather_tile(const LineArgs& a, long long tile, long long ntiles, int
 }
 
 // Unit-cell gradients of the nodal line values u0 (last axis, already masked)
-// of the warp's cells: Gx in registers
-// (x-line owners), the axis-1 derivative in buffer g1, axis-2 (3D) in g2.
-// Buffers a and b are scratch.
+// of the warp's cells: Gx in registers (x-line owners), the axis-1 derivative
+// in buffer g1, the axis-2 derivative (3D) in g2.  a and b are scratch; g1 may
+// be a (the y-derivative then overwrites the values in place, line by line,
+// after the z-lines have read them) and g2 may be b.
 template <int DIM, int N>
 HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live, const LineOff<DIM, N>& t,
                       double* a, double* b, double* g1, double* g2, double (&Gx)[DIM][N]) {
@@ -294,15 +295,18 @@ HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live
     for (int c = 0; c < DIM; ++c) c1d<N, false>(T.Dc, u[c], Gx[c]);
   }
   __syncwarp();
-  if (live) {
-    ld_line<DIM, N, 1>(a, t, u);
-    c_line<DIM, N, false>(T.Dc, u);
-    st_line<DIM, N, 1>(g1, t, u);
-    if (DIM == 3) {
+  if (DIM == 3) {
+    if (live) {
       ld_line<DIM, N, DIM - 1>(a, t, u);
       c_line<DIM, N, false>(T.Dc, u);
       st_line<DIM, N, DIM - 1>(g2, t, u);
     }
+    if (g1 == a) __syncwarp();  // the y-lines overwrite sites the z-lines read
+  }
+  if (live) {
+    ld_line<DIM, N, 1>(a, t, u);
+    c_line<DIM, N, false>(T.Dc, u);
+    st_line<DIM, N, 1>(g1, t, u);
   }
   __syncwarp();
 }
@@ -350,7 +354,16 @@ HF_DEV void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned lon
 template <int DIM, int N, int VAR, typename ST = double>
 struct LinePlan {
   using K = LineCfg<DIM, N>;
-  static constexpr int NB = (VAR == SCALAR) ? 5 : 3;
+  // line buffers: A (values at the Gauss points, finally the integration
+  // result) and B (scratch, then G2 and the queued z part).  The queued x part
+  // stays in the x-line owner's registers (XREG, and G1 overwrites the values
+  // in A in place) or replaces the values in A (and G1 takes a third buffer).  XREG measured faster for tensor2 and scalar at Q2
+  // (tensor2 b2b 47.7 -> 44.4 us: the smaller slice admits a 12th warp) and
+  // slower for tensor4 (55.6 -> 56.4 us at 7 warps, 59 us at the 8 warps the
+  // freed buffer admits); at Q4 the 15 extra registers spill.  The scalar
+  // strategy adds two buffers for the gradients of ubar.
+  static constexpr bool XREG = N <= 3 && VAR != TENSOR4;
+  static constexpr int NB = (XREG ? 2 : 3) + (VAR == SCALAR ? 2 : 0);
   static constexpr int NF = (VAR == SCALAR) ? 2 + DIM * DIM : CacheFields<DIM, VAR>::NF;
   // ST elements per (tile, iq) chunk (fp64, or the fp32 storage of a mixed-precision level)
   static constexpr long long CH = TileLayout<DIM, N>::template chunk_e<sizeof(ST)>(NF);
@@ -424,10 +437,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   double* bufs[NB];
 #pragma unroll
   for (int b = 0; b < NB; ++b) bufs[b] = wb + b * Y::BUF;
-  double* Q = DIM == 3 ? bufs[0] : bufs[1];   // Q, later the x part of the queued data
-  double* Sc = DIM == 3 ? bufs[1] : bufs[0];  // scratch of the evaluation
-  double* G1 = DIM == 3 ? bufs[1] : bufs[0];
-  double* G2 = bufs[2];
+  double* A = bufs[0];  // values at the Gauss points -> G1 (in place) -> queued y part -> result
+  double* B = bufs[1];  // scratch -> G2 -> queued z part
 
   long long jc = 0;  // this warp's chunk counter
   const long long tstep = (long long)W * gridDim.x;
@@ -446,8 +457,14 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 
     double Gx[DIM][N];
     double Gxu[DIM][N];  // scalar: x part of the gradient of ubar
-    if (VAR == SCALAR) eval_line<DIM, N>(T, g.ub, live, lo, Q, Sc, bufs[3], bufs[4], Gxu);
-    eval_line<DIM, N>(T, u, live, lo, Q, Sc, G1, G2, Gx);
+    if (VAR == SCALAR) eval_line<DIM, N>(T, g.ub, live, lo, A, B, bufs[NB - 2], bufs[NB - 1], Gxu);
+    // XREG: G1 overwrites the values in A in place; else G1 goes to the third
+    // buffer and the queued x part later replaces the values in A
+    double* G1 = PL::XREG ? A : bufs[2];
+    double* G2 = B;
+    double* X = A;
+    double vx[DIM][N];  // queued x part of this thread's x-line (XREG)
+    eval_line<DIM, N>(T, u, live, lo, A, B, G1, G2, Gx);
 
     // ---------------- P: q-point physics along this thread's x-line ----------------
     double mu = 0.0, lam = 0.0;
@@ -501,8 +518,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc) {
           gub[cc][0] = Gxu[cc][iq];
-          gub[cc][1] = bufs[3][cc * Y::CS + pt];
-          if (DIM == 3) gub[cc][DIM - 1] = bufs[4][cc * Y::CS + pt];
+          gub[cc][1] = bufs[NB - 2][cc * Y::CS + pt];
+          if (DIM == 3) gub[cc][DIM - 1] = bufs[NB - 1][cc * Y::CS + pt];
         }
         double F[DIM * DIM];
 #pragma unroll
@@ -539,7 +556,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       }
 #pragma unroll
       for (int cc = 0; cc < DIM; ++cc) {
-        Q[cc * Y::CS + pt] = G[cc][0];
+        if (PL::XREG)
+          vx[cc][iq] = G[cc][0];
+        else
+          X[cc * Y::CS + pt] = G[cc][0];
         G1[cc * Y::CS + pt] = G[cc][1];
         if (DIM == 3) G2[cc * Y::CS + pt] = G[cc][DIM - 1];
       }
@@ -572,12 +592,16 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       }
     }
     __syncwarp();
-    // ---------------- I1: transposed collocation derivative per axis, in place ----------------
+    // ---------------- I1: transposed collocation derivative per axis (x in registers, y/z in place) ----------------
     if (live) {
       double v[DIM][N];
-      ld_line<DIM, N, 0>(Q, lo, v);
-      c_line<DIM, N, true>(T.Dc, v);
-      st_line<DIM, N, 0>(Q, lo, v);
+      if (PL::XREG) {
+        c_line<DIM, N, true>(T.Dc, vx);
+      } else {
+        ld_line<DIM, N, 0>(X, lo, v);
+        c_line<DIM, N, true>(T.Dc, v);
+        st_line<DIM, N, 0>(X, lo, v);
+      }
       ld_line<DIM, N, 1>(G1, lo, v);
       c_line<DIM, N, true>(T.Dc, v);
       st_line<DIM, N, 1>(G1, lo, v);
@@ -591,7 +615,14 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     // ---------------- I2: sum, transposed interpolation along x ----------------
     if (live) {
       double v[DIM][N], w[DIM][N];
-      ld_line<DIM, N, 0>(Q, lo, v);
+      if (PL::XREG) {
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc)
+#pragma unroll
+          for (int l = 0; l < N; ++l) v[cc][l] = vx[cc][l];
+      } else {
+        ld_line<DIM, N, 0>(X, lo, v);
+      }
       ld_line<DIM, N, 0>(G1, lo, w);
 #pragma unroll
       for (int cc = 0; cc < DIM; ++cc)
@@ -605,15 +636,15 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
           for (int l = 0; l < N; ++l) v[cc][l] += w[cc][l];
       }
       c_line<DIM, N, true>(T.V, v);
-      st_line<DIM, N, 0>(Q, lo, v);
+      st_line<DIM, N, 0>(A, lo, v);
     }
     __syncwarp();
     if (DIM == 3) {
       if (live) {
         double v[DIM][N];
-        ld_line<DIM, N, 1>(Q, lo, v);
+        ld_line<DIM, N, 1>(A, lo, v);
         c_line<DIM, N, true>(T.V, v);
-        st_line<DIM, N, 1>(Q, lo, v);
+        st_line<DIM, N, 1>(A, lo, v);
       }
       __syncwarp();
     }
@@ -624,7 +655,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     }
     if (live) {
       double v[DIM][N];
-      ld_line<DIM, N, DIM - 1>(Q, lo, v);
+      ld_line<DIM, N, DIM - 1>(A, lo, v);
       c_line<DIM, N, true>(T.V, v);
       unsigned nb, s_last;
       last_axis_line<DIM, N>(a.lat, g.node0, t, nb, s_last);
