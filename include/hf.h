@@ -125,6 +125,12 @@ HF_API int hf_tangent_apply_after_fill(hf_tangent* op, const double* x_dev, doub
 HF_API int hf_tangent_tiles(const hf_tangent* op, long long* n_tiles, int* cells_per_tile);
 HF_API int hf_tangent_apply_tiles(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
                                   long long tile0, long long tile1, int mode, void* stream);
+/* the same, launched on reserve_sms fewer SMs: the interior tiles of a slab
+ * run while the interface exchange (an NCCL kernel on another stream) is in
+ * flight, and a persistent block that cannot start beside the NCCL kernel
+ * would otherwise finish late by the whole exchange */
+HF_API int hf_tangent_apply_tiles_ex(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                     long long tile0, long long tile1, int mode, int reserve_sms, void* stream);
 /* Host-to-host .apply for callers that hold the vectors in host memory (the
  * reference's numpy arrays, operators.py:331-339): y_host = A x_host.  Both
  * buffers must be page-locked (cudaHostAlloc / pinned torch tensors, or

@@ -493,7 +493,7 @@ HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev,
 }
 
 static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev, int fill,
-                         void* stream, long long tile0 = 0, long long tile1 = -1) {
+                         void* stream, long long tile0 = 0, long long tile1 = -1, int reserve_sms = 0) {
   if (!op || !x_dev || !y_dev) return fail(HF_ERR_ARG, "null argument");
   CellArgs a = base_args(op->sp);
   a.tile0 = tile0;
@@ -506,6 +506,7 @@ static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, con
   a.ubar = op->d_ubar;
   a.skip = skip_dev;
   a.fill = fill;
+  a.reserve_sms = reserve_sms;
   HF_CUDA(cell(op->sp, OP_APPLY, op->strategy, a, S(stream)));
   return HF_OK;
 }
@@ -559,6 +560,14 @@ HF_API int hf_tangent_apply_tiles(hf_tangent* op, const double* x_dev, double* y
   if (mode < 0 || mode > 2 || tile0 < 0 || tile1 < tile0) return fail(HF_ERR_ARG, "bad tile range or mode");
   if (!op || op->sp->lat.n_el == 0 || tile1 == tile0) return op ? HF_OK : fail(HF_ERR_ARG, "null tangent");
   return tangent_apply(op, x_dev, y_dev, skip_dev, mode, stream, tile0, tile1);
+}
+
+HF_API int hf_tangent_apply_tiles_ex(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev,
+                                     long long tile0, long long tile1, int mode, int reserve_sms, void* stream) {
+  if (mode < 0 || mode > 2 || tile0 < 0 || tile1 < tile0 || reserve_sms < 0)
+    return fail(HF_ERR_ARG, "bad tile range, mode or reserve");
+  if (!op || op->sp->lat.n_el == 0 || tile1 == tile0) return op ? HF_OK : fail(HF_ERR_ARG, "null tangent");
+  return tangent_apply(op, x_dev, y_dev, skip_dev, mode, stream, tile0, tile1, reserve_sms);
 }
 
 HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream) {

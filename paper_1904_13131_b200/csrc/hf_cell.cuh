@@ -69,6 +69,7 @@ struct CellArgs {
   int fp32;                 // apply/build: cache and x/y stored as float (mixed-precision levels)
   long long cache_len;      // cache elements (bounds checks of the debug build)
   long long tile0, tile1;   // apply: tile range; tile1 < 0 means all tiles
+  int reserve_sms = 0;      // apply: leave this many SMs' worth of blocks free (a concurrent NCCL kernel)
   unsigned long long* detmin;  // ordered-double min of det F (build / residual / range)
   unsigned long long* detmax;
 };

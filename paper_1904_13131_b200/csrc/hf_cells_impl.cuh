@@ -6,6 +6,16 @@
 
 namespace hf {
 
+inline int nsm_cached() {
+  static int n = -1;
+  if (n < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
 // Launch of the line-parallel apply (hf_line.cuh): persistent warps, grid
 // sized to the resident capacity (148 SMs x blocks per SM) or the tile count.
 template <int DIM, int N, int VAR, typename ST>
@@ -58,7 +68,9 @@ cudaError_t launch_apply_line_t(const CellArgs& c, cudaStream_t s) {
   // which shortens its latency chain; larger levels fill every SM.
   const long long tiles = a.tile1 - a.tile0;
   long long nb = tiles;
-  if (nb > resident) nb = resident;
+  long long cap = resident;
+  if (c.reserve_sms > 0 && cap > 2ll * c.reserve_sms) cap -= (cap / (nsm_cached() > 0 ? nsm_cached() : 148)) * c.reserve_sms;
+  if (nb > cap) nb = cap;
   if (nb <= 0) return cudaSuccess;
   if (!c.fill) {
     k_apply_line<DIM, N, VAR, ST><<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);

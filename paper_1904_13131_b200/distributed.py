@@ -31,6 +31,7 @@ ranks on one GPU in the tests), ``LocalComm`` for one rank.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 
@@ -84,6 +85,15 @@ class _Works:
     def wait(self):
         for w in self.works:
             w.wait()
+
+
+def _nccl_sms(exchange) -> int:
+    """SMs left to a concurrent NCCL exchange kernel (HF_NCCL_SMS, default 4);
+    0 for host-staged transports."""
+    comm = getattr(exchange, "comm", None)
+    if comm is None or getattr(comm, "staged", True):
+        return 0
+    return int(os.environ.get("HF_NCCL_SMS", "4"))
 
 
 class TorchComm:
@@ -442,7 +452,9 @@ class DistributedTangent:
         ex = self.dp.exchange
         with ex.timer.span("exchange"):
             h = ex.start(y)
-        self.local.apply_tiles(x, y, i0, i1, mode=0)
+        # while NCCL's kernel holds a few SMs, launch the persistent interior
+        # blocks on the others (a block queued behind it would finish late)
+        self.local.apply_tiles(x, y, i0, i1, mode=0, reserve_sms=_nccl_sms(ex))
         with ex.timer.span("exchange"):
             ex.finish(h, y)
         return y

@@ -335,10 +335,13 @@ class MatrixFreeTangent:
         check(lib().hf_tangent_tiles(self._op, ct.byref(nt), ct.byref(cpt)))
         return nt.value, cpt.value
 
-    def apply_tiles(self, x: torch.Tensor, y: torch.Tensor, tile0: int, tile1: int, mode: int = 0) -> torch.Tensor:
+    def apply_tiles(self, x: torch.Tensor, y: torch.Tensor, tile0: int, tile1: int, mode: int = 0,
+                    reserve_sms: int = 0) -> torch.Tensor:
         """y += A_loc x over the cells of tiles [tile0, tile1) (constrained rows dropped);
-        mode 1/2: programmatic dependent of the fill / of an x-and-y producer."""
-        check(lib().hf_tangent_apply_tiles(self._op, dv.ptr(x), dv.ptr(y), None, tile0, tile1, mode, dv.stream()))
+        mode 1/2: programmatic dependent of the fill / of an x-and-y producer;
+        reserve_sms: launch on that many fewer SMs (a concurrent NCCL kernel)."""
+        check(lib().hf_tangent_apply_tiles_ex(self._op, dv.ptr(x), dv.ptr(y), None, tile0, tile1, mode, reserve_sms,
+                                              dv.stream()))
         return y
 
     def apply_raw(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:

@@ -136,3 +136,25 @@ def test_host_apply_graph_chunks_and_buffers(cfg, m):
     finally:
         check(lib().hf_host_unregister(ct.c_void_p(xa.ctypes.data)))
         check(lib().hf_host_unregister(ct.c_void_p(ya.ctypes.data)))
+
+
+def test_tile_range_apply_with_reserved_sms():
+    """hf_tangent_apply_tiles_ex: tile ranges launched on fewer SMs (room for a
+    concurrent NCCL kernel) accumulate the same result as the full apply."""
+    from paper_1904_13131_b200 import MatrixFreeTangent
+    from paper_1904_13131_b200._lib import check, lib
+    from paper_1904_13131_b200 import device as dv
+    from paper_1904_13131_b200.workloads import make_workload
+
+    wl = make_workload(2, seed=6, m=12)
+    op = MatrixFreeTangent(wl.fine, wl.ubar, "tensor4")
+    x = torch.from_numpy(wl.x).cuda()
+    ref = op.apply(x)
+    nt, _ = op.tiles()
+    for reserve in (0, 4, 100):
+        y = torch.empty_like(x)
+        check(lib().hf_fill_masked(x.numel(), dv.ptr(y), dv.ptr(x), dv.ptr(wl.fine.mask_dev), 0.0, dv.stream()))
+        cut = nt // 3
+        op.apply_tiles(x, y, 0, cut, reserve_sms=reserve)
+        op.apply_tiles(x, y, cut, nt, reserve_sms=reserve)
+        assert _rel(y, ref) < 1e-14
