@@ -537,11 +537,13 @@ def build_transfers(problems):
 def build_level_operators(problems, u_fine, strategy: str = "tensor4", seed: int = 0, keep_constrained: bool = False,
                           coarse_precision: str = "fp64"):
     """Linearise every level at the injected fine displacement (multigrid.py:358-369);
-    ``coarse_precision="fp32"`` runs every level below the finest in fp32 storage."""
+    ``coarse_precision="fp32"`` runs the levels between the finest and the
+    coarsest in fp32 storage.  The coarsest stays fp64: it is latency bound
+    (halving its bytes gains nothing) and runs the one-kernel coarse solve."""
     u_levels = restrict_solution(problems, dv.as_dev(u_fine), keep_constrained)
     top = len(problems) - 1
     return [LevelOperator(p, u, strategy, seed=seed + 7919 * lvl, level=lvl, is_coarsest=(lvl == 0),
-                          precision=coarse_precision if lvl < top else "fp64")
+                          precision=coarse_precision if 0 < lvl < top else "fp64")
             for lvl, (p, u) in enumerate(zip(problems, u_levels))]
 
 

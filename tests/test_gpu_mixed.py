@@ -67,8 +67,8 @@ def test_gmg_cg_with_fp32_levels(name):
     probs = product_levels(g)
     op = MatrixFreeTangent(probs[-1], g["ubar"], str(g["strategy"]))
     gmg = build_gmg(probs, g["ubar"], str(g["strategy"]), seed=0, coarse_precision="fp32")
-    assert all(lv.x.dtype == torch.float32 for lv in gmg.levels[:-1])
-    assert gmg.levels[-1].x.dtype == torch.float64
+    assert all(lv.x.dtype == torch.float32 for lv in gmg.levels[1:-1])
+    assert gmg.levels[-1].x.dtype == torch.float64 and gmg.levels[0].x.dtype == torch.float64
     x, rep = cg(op, g["b"], rel_tol=1e-8, preconditioner=gmg)
     assert rep.converged
     assert rep.iterations <= int(g["cg_iterations"]) + 2
