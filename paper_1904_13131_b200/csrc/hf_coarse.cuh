@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(COARSE_THREADS) k_coarse_cheb(const CoarseArgs
   const unsigned char* gb = a.blob + a.boff[blockIdx.x];
   const CoarseBlock hb = *reinterpret_cast<const CoarseBlock*>(gb);
   const int r0 = hb.r0, r1 = hb.r0 + hb.rows, nu = hb.nu, nnz = hb.nnz;
+  HF_ASSERT(r0 >= 0 && r1 <= a.n && nu >= 0 && nnz >= 0);
   // copy the block body to shared memory (16-byte vectors)
   const size_t body = coarse_align16(8ull * nnz) + coarse_align16(4ull * nu) + coarse_align16(4ull * (hb.rows + 1)) +
                       coarse_align16(2ull * nnz);
@@ -143,14 +144,21 @@ __global__ void __launch_bounds__(COARSE_THREADS) k_coarse_cheb(const CoarseArgs
     const double rho = 1.0 / (2.0 * a.sigma - rho_old);
     const double cd = rho * rho_old, cz = 2.0 * rho / a.delta;
     // gather the iterate entries this CTA's rows touch (one L2 round trip)
-    for (int j = threadIdx.x; j < nu; j += blockDim.x) xs[j] = __ldcg(xin + ucol[j]);
+    for (int j = threadIdx.x; j < nu; j += blockDim.x) {
+      HF_ASSERT(ucol[j] >= 0 && ucol[j] < a.n);
+      xs[j] = __ldcg(xin + ucol[j]);
+    }
     __syncthreads();
     // (A x)_i of this CTA's rows from shared memory, one warp per row
     double rr = 0.0;
     for (int l = warp; l < hb.rows; l += nw) {
       const int k0 = rowptr[l], k1 = rowptr[l + 1];
       double s = 0.0;
-      for (int k = k0 + lane; k < k1; k += 32) s = fma(val[k], xs[lcol[k]], s);
+      HF_ASSERT(k0 >= 0 && k1 <= nnz && k0 <= k1);
+      for (int k = k0 + lane; k < k1; k += 32) {
+        HF_ASSERT(lcol[k] < nu);
+        s = fma(val[k], xs[lcol[k]], s);
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) {
@@ -197,7 +205,11 @@ __global__ void k_coarse_values(int nupd, const int* __restrict__ cptr, const in
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= nupd) return;
   double v = 0.0;
-  for (int k = cptr[u]; k < cptr[u + 1]; ++k) v += elem[cidx[k]];
+  for (int k = cptr[u]; k < cptr[u + 1]; ++k) {
+    HF_ASSERT(cidx[k] >= 0);
+    v += elem[cidx[k]];
+  }
+  HF_ASSERT(uoff[u] >= 16 && (uoff[u] & 7) == 0);
   *reinterpret_cast<double*>(blob + uoff[u]) = v;
 }
 
