@@ -663,9 +663,11 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       for (int l = 0; l < N; ++l) {
         const unsigned d0 = (nb + l * s_last) * DIM;
         HF_ASSERT((long long)d0 + DIM <= a.lat.n_nodes * DIM);
+        // constrained rows take +0 (their identity value x is unchanged):
+        // no branch per DoF around the reductions
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc)
-          if (!((g.mb >> (cc * N + l)) & 1u)) atomicAdd(reinterpret_cast<ST*>(a.y) + d0 + cc, (ST)v[cc][l]);
+          atomicAdd(reinterpret_cast<ST*>(a.y) + d0 + cc, ((g.mb >> (cc * N + l)) & 1u) ? (ST)0 : (ST)v[cc][l]);
       }
     }
     __syncwarp();  // line buffers are reused by the next tile
