@@ -360,6 +360,9 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": ab / kern_ms / 1e6, "peak": hbm, "unit": "GB/s",
                          "frac": ab / kern_ms / 1e6 / hbm, "traffic": traffic["bytes_per_launch"] if traffic else None,
                          "peak_source": peak_kind, "algorithmic_bytes_per_launch": ab,
+                         "algorithmic_bytes_note": "8 (2 N_dof + 36 N_qp): this design's tensor4 cache folds JxW into "
+                                                   "tau and M (SURVEY's P = 37 stores it: "
+                                                   f"{algorithmic_bytes('tensor4', 3, prob.n_dofs, nqp, True)} B)",
                          "kernel_ms": kern_ms, "kernel": KERNEL},
             "e2e": {"value": n_global / e2e_ms / 1e6, "unit": "GDoF/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,

@@ -394,8 +394,8 @@ static cudaError_t cell(const hf_space* sp, int op, int var, const CellArgs& a, 
 
 static int nfields(int dim, int strategy) {
   int nv = dim * (dim + 1) / 2, nm = nv * (nv + 1) / 2;
-  if (strategy == HF_TENSOR4) return nv + nm + dim * dim + 1;
-  if (strategy == HF_TENSOR2) return 2 + nv + dim * dim + 1;
+  if (strategy == HF_TENSOR4) return nv + nm + dim * dim;  // JxW folded into tau, M (CacheFields)
+  if (strategy == HF_TENSOR2) return 2 + nv + dim * dim;
   return 2 + dim * dim;  // c1 + J^-1 + JxW (tile layout, hf_line.cuh)
 }
 

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256) k_assemble_local(const CellArgs a, double
   constexpr int NQ = Cfg<DIM, N>::NQ;  // nloc == nq
   constexpr int NV = DIM * (DIM + 1) / 2;
   constexpr int NM = NV * (NV + 1) / 2;
-  constexpr int NF = NV + NM + DIM * DIM + 1;  // tensor4 cache fields
+  constexpr int NF = CacheFields<DIM, TENSOR4>::NF;  // tensor4 cache fields (JxW folded in)
   constexpr int NLD = NQ * DIM;
   __shared__ double gs[NQ][NQ][DIM];  // [q][n][j]
   __shared__ double Mq[NQ][NV][NV];
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) k_assemble_local(const CellArgs a, double
       }
     for (int r = 0; r < NV; ++r)
       for (int c = 0; c < NV; ++c) Mq[q][r][c] = f[NV + (r <= c ? hf_triu<NV>(r, c) : hf_triu<NV>(c, r))];
-    wq[q] = f[NF - 1];
+    wq[q] = 1.0;  // JxW is folded into the cached tau and M (CacheFields)
   }
   __syncthreads();
   // spatial gradients of every node basis at every q-point

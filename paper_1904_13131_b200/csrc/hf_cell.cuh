@@ -43,10 +43,14 @@ template <int DIM, int VAR>
 struct CacheFields {
   static constexpr int NV = DIM * (DIM + 1) / 2;
   static constexpr int NM = NV * (NV + 1) / 2;
-  // tensor4: tau(NV) M(NM) sinv(D*D) JxW ; tensor2: c1 c2 tau(NV) sinv JxW ;
-  // scalar: c1 J^-1(D*D) JxW (the geometry it re-reads, stored beside c1 in the tile layout)
-  static constexpr int NF = VAR == TENSOR4 ? NV + NM + DIM * DIM + 1
-                                           : (VAR == TENSOR2 ? 2 + NV + DIM * DIM + 1 : 2 + DIM * DIM);
+  // tensor4: JxW tau(NV), JxW M(NM), sinv(D*D) ; tensor2: JxW 2c1, JxW 2lambda, JxW tau(NV), sinv ;
+  // scalar: c1 J^-1(D*D) JxW (the geometry it re-reads, stored beside c1 in the tile layout).
+  // tensor4/tensor2 fold the quadrature weight JxW into the fields the q-point
+  // action is linear in (deal.II's practice), so it is neither stored nor
+  // multiplied per point: 36 / 17 doubles per q-point instead of the
+  // reference's 37 / 18 (operators.py:259-289 keep JxW in the geometry).
+  static constexpr int NF = VAR == TENSOR4 ? NV + NM + DIM * DIM
+                                           : (VAR == TENSOR2 ? 2 + NV + DIM * DIM : 2 + DIM * DIM);
 };
 
 struct CellArgs {
@@ -456,15 +460,16 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_build(const CellArgs a) {
     put(f++, __ldg(a.jxw + qi));
     return;
   }
+  const double w = __ldg(a.jxw + qi);  // folded into the fields below (CacheFields)
   if (VAR == TENSOR2) {
-    put(f++, 2.0 * k.c1);
-    put(f++, 2.0 * lam);
+    put(f++, w * (2.0 * k.c1));
+    put(f++, w * (2.0 * lam));
   }
 #pragma unroll
   for (int s = 0; s < NV; ++s) {
     int i = s < DIM ? s : (DIM == 2 ? 0 : (s == 3 ? 1 : 0));
     int j = s < DIM ? s : (DIM == 2 ? 1 : (s == 5 ? 1 : 2));
-    put(f++, k.tau[i][j]);
+    put(f++, w * k.tau[i][j]);
   }
   if (VAR == TENSOR4) {
     // Voigt matrix of J c (material.py:195-208), packed upper (218-222)
@@ -475,14 +480,13 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_build(const CellArgs a) {
         double v = 0.0;
         if (r < DIM && c < DIM) v = 2.0 * lam + (r == c ? 2.0 * k.c1 : 0.0);
         else if (r == c) v = k.c1;
-        put(f++, v);
+        put(f++, w * v);
       }
   }
 #pragma unroll
   for (int r = 0; r < DIM; ++r)
 #pragma unroll
     for (int c = 0; c < DIM; ++c) put(f++, k.sinv[r][c]);
-  put(f++, __ldg(a.jxw + qi));
 }
 
 // ---------------------------------------------------------------------------
@@ -548,7 +552,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_diag(const CellArgs a) {
         tau[i][j] = cf[off + hf_slot<DIM>(i, j)];
         sinv[i][j] = cf[off + NV + (VAR == TENSOR4 ? K::NM : 0) + i * DIM + j];
       }
-    jxw = cf[NF - 1];
+    jxw = 1.0;  // folded into the cached fields (CacheFields)
 #pragma unroll
     for (int c = 0; c < DIM; ++c)
 #pragma unroll

@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
             tau[i][j] = f[hf_slot<DIM>(i, j)];
             sinv[i][j] = f[NV + NM + i * DIM + j];
           }
-        qp_action<DIM, true>(gu, sinv, tau, 0.0, 0.0, f + NV, f[NF - 1], G);
+        qp_action<DIM, true>(gu, sinv, tau, 0.0, 0.0, f + NV, 1.0, G);  // JxW folded into tau, M
       } else if (VAR == TENSOR2) {
         double sinv[DIM][DIM], tau[DIM][DIM];
 #pragma unroll
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
             tau[i][j] = f[2 + hf_slot<DIM>(i, j)];
             sinv[i][j] = f[2 + NV + i * DIM + j];
           }
-        qp_action<DIM, false>(gu, sinv, tau, f[0], f[1], nullptr, f[NF - 1], G);
+        qp_action<DIM, false>(gu, sinv, tau, f[0], f[1], nullptr, 1.0, G);  // JxW folded into c1', c2', tau
       } else {
         // rebuild F, b, tau = mu b - c1 I and s_inv from ubar (operators.py:349-363)
         double ji[DIM][DIM];

@@ -192,10 +192,13 @@ def stack_mesh(mesh, k: int):
     return replace(mesh, cells=cells, vertices=np.ascontiguousarray(verts), material_id=mat)
 
 
-def algorithmic_bytes(strategy: str, dim: int, n_dofs: int, n_qp: int) -> int:
-    """Bytes one apply must move: 8 (v N_dof + P N_qp)."""
+def algorithmic_bytes(strategy: str, dim: int, n_dofs: int, n_qp: int, reference_fields: bool = False) -> int:
+    """Bytes one apply must move: 8 (v N_dof + P N_qp).  The
+    cache of this design folds JxW into the tensor4 / tensor2 fields (P = 36 /
+    17 in 3D); ``reference_fields`` gives SURVEY's P = 37 / 18 (JxW stored)."""
     nv = dim * (dim + 1) // 2
-    P = {"tensor4": nv + nv * (nv + 1) // 2 + dim * dim + 1, "tensor2": 2 + nv + dim * dim + 1,
+    jxw = 1 if reference_fields else 0
+    P = {"tensor4": nv + nv * (nv + 1) // 2 + dim * dim + jxw, "tensor2": 2 + nv + dim * dim + jxw,
          "scalar": 1 + dim * dim + 1}[strategy]
     v = 3 if strategy == "scalar" else 2
     return 8 * (v * n_dofs + P * n_qp)

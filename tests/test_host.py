@@ -60,10 +60,14 @@ def test_meter_flops_matches_reference_count(name):
 
 
 def test_algorithmic_bytes_survey_formula():
-    # cfg2 tensor4 333.9 B/DoF, tensor2 170.6, scalar 118.5
+    # cfg2 tensor4 333.9 B/DoF, tensor2 170.6, scalar 118.5 (JxW stored)
     nd, nqp = 823875, 32**3 * 27
     for s, bpd in (("tensor4", 333.9), ("tensor2", 170.6), ("scalar", 118.5)):
-        assert abs(workloads.algorithmic_bytes(s, 3, nd, nqp) / nd - bpd) < 0.05
+        assert abs(workloads.algorithmic_bytes(s, 3, nd, nqp, reference_fields=True) / nd - bpd) < 0.05
+    # this design folds JxW into the tensor4 / tensor2 fields: one double less per q-point
+    for s in ("tensor4", "tensor2"):
+        assert workloads.algorithmic_bytes(s, 3, nd, nqp, True) - workloads.algorithmic_bytes(s, 3, nd, nqp) == 8 * nqp
+    assert workloads.algorithmic_bytes("scalar", 3, nd, nqp, True) == workloads.algorithmic_bytes("scalar", 3, nd, nqp)
 
 
 def test_workload_recipe():
