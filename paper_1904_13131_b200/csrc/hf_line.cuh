@@ -311,6 +311,77 @@ HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live
   __syncwarp();
 }
 
+// eval_line for two fields at once (the scalar strategy's x and ubar): every
+// axis phase handles both, so the evaluation takes half the phases and each
+// phase has twice the independent work.  Field 1 uses scratch a, b and writes
+// g1, g2 (g1 may be a); field 2 uses c, d and writes its y-derivative in place
+// in c and its z-derivative in d.
+template <int DIM, int N>
+HF_DEV void eval_line2(const TabLine<N>& T, const double (&u0)[DIM][N], const double (&w0)[DIM][N], bool live,
+                       const LineOff<DIM, N>& t, double* a, double* b, double* g1, double* g2, double* c, double* d,
+                       double (&Gx)[DIM][N], double (&Gw)[DIM][N]) {
+  double u[DIM][N], w[DIM][N];
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        u[k][l] = u0[k][l];
+        w[k][l] = w0[k][l];
+      }
+    c_line<DIM, N, false>(T.V, u);
+    c_line<DIM, N, false>(T.V, w);
+    st_line<DIM, N, DIM - 1>(DIM == 3 ? a : b, t, u);
+    st_line<DIM, N, DIM - 1>(DIM == 3 ? c : d, t, w);
+  }
+  __syncwarp();
+  if (DIM == 3) {
+    if (live) {
+      ld_line<DIM, N, 1>(a, t, u);
+      ld_line<DIM, N, 1>(c, t, w);
+      c_line<DIM, N, false>(T.V, u);
+      c_line<DIM, N, false>(T.V, w);
+      st_line<DIM, N, 1>(b, t, u);
+      st_line<DIM, N, 1>(d, t, w);
+    }
+    __syncwarp();
+  }
+  if (live) {
+    ld_line<DIM, N, 0>(b, t, u);
+    ld_line<DIM, N, 0>(d, t, w);
+    c_line<DIM, N, false>(T.V, u);
+    c_line<DIM, N, false>(T.V, w);
+    st_line<DIM, N, 0>(a, t, u);
+    st_line<DIM, N, 0>(c, t, w);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      c1d<N, false>(T.Dc, u[k], Gx[k]);
+      c1d<N, false>(T.Dc, w[k], Gw[k]);
+    }
+  }
+  __syncwarp();
+  if (DIM == 3) {
+    if (live) {
+      ld_line<DIM, N, DIM - 1>(a, t, u);
+      ld_line<DIM, N, DIM - 1>(c, t, w);
+      c_line<DIM, N, false>(T.Dc, u);
+      c_line<DIM, N, false>(T.Dc, w);
+      st_line<DIM, N, DIM - 1>(g2, t, u);
+      st_line<DIM, N, DIM - 1>(d, t, w);
+    }
+    __syncwarp();  // the y-lines overwrite sites the z-lines read (c always, a when g1 == a)
+  }
+  if (live) {
+    ld_line<DIM, N, 1>(a, t, u);
+    ld_line<DIM, N, 1>(c, t, w);
+    c_line<DIM, N, false>(T.Dc, u);
+    c_line<DIM, N, false>(T.Dc, w);
+    st_line<DIM, N, 1>(g1, t, u);
+    st_line<DIM, N, 1>(c, t, w);
+  }
+  __syncwarp();
+}
+
 // ---- mbarrier / TMA bulk-copy primitives (PTX) ----
 HF_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 HF_DEV void mbar_init(unsigned long long* b, unsigned count) {
@@ -457,14 +528,21 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 
     double Gx[DIM][N];
     double Gxu[DIM][N];  // scalar: x part of the gradient of ubar
-    if (VAR == SCALAR) eval_line<DIM, N>(T, g.ub, live, lo, A, B, bufs[NB - 2], bufs[NB - 1], Gxu);
     // XREG: G1 overwrites the values in A in place; else G1 goes to the third
     // buffer and the queued x part later replaces the values in A
     double* G1 = PL::XREG ? A : bufs[2];
     double* G2 = B;
     double* X = A;
     double vx[DIM][N];  // queued x part of this thread's x-line (XREG)
-    eval_line<DIM, N>(T, u, live, lo, A, B, G1, G2, Gx);
+    // scalar: gradients of x and ubar in one pass (ubar's land in bufs[NB-2]
+    // (y) and bufs[NB-1] (z)); above Q4 the doubled line registers spill, so
+    // the two fields are evaluated one after the other there
+    constexpr bool FUSED = VAR == SCALAR && N <= 5;
+    if (VAR == SCALAR && !FUSED) eval_line<DIM, N>(T, g.ub, live, lo, A, B, bufs[NB - 2], bufs[NB - 1], Gxu);
+    if (FUSED)
+      eval_line2<DIM, N>(T, u, g.ub, live, lo, A, B, G1, G2, bufs[NB - 2], bufs[NB - 1], Gx, Gxu);
+    else
+      eval_line<DIM, N>(T, u, live, lo, A, B, G1, G2, Gx);
 
     // ---------------- P: q-point physics along this thread's x-line ----------------
     double mu = 0.0, lam = 0.0;
