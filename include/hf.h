@@ -156,6 +156,12 @@ HF_API int hf_tangent_host_info(const hf_tangent* op, int* variant, float* us4);
 /* page-lock / release caller-owned host memory (cudaHostRegister) */
 HF_API int hf_host_register(void* host_ptr, long long bytes);
 HF_API int hf_host_unregister(void* host_ptr);
+/* Alternate the direction of successive whole-range applies (forwards,
+ * backwards, ...): a sweep then starts on the q-point cache tiles the previous
+ * one read last, which a 126 MB L2 may still hold.  Off by default (the
+ * single-apply benchmark streams the cache); the multigrid levels turn it on
+ * for their smoother sweeps.  Results change only by summation order. */
+HF_API int hf_tangent_set_alternate(hf_tangent* op, int on);
 /* matrix-based baseline (assemble_matrix / AssembledTangent, operators.py:436-516):
  * vals_dev (n_el, nld, nld) element matrices of a tensor4 tangent, nld = nloc*dim,
  * local DoF n*dim + c; dofs_dev (n_el, nld) their global DoFs (operators.py:474).

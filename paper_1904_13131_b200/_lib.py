@@ -52,6 +52,7 @@ _SIGS = {
     "hf_tangent_tiles": (I, [P, ct.POINTER(LL), ct.POINTER(I)]),
     "hf_tangent_apply_tiles": (I, [P, P, P, P, LL, LL, I, P]),
     "hf_tangent_apply_tiles_ex": (I, [P, P, P, P, LL, LL, I, I, P]),
+    "hf_tangent_set_alternate": (I, [P, I]),
     "hf_tangent_apply_host": (I, [P, P, P, I, P]),
     "hf_host_register": (I, [P, LL]),
     "hf_tangent_host_info": (I, [P, ct.POINTER(I), ct.POINTER(ct.c_float)]),

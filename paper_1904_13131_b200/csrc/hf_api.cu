@@ -120,6 +120,8 @@ struct hf_tangent {
   double* d_cache = nullptr;
   double* d_ubar = nullptr;
   HostPipe* host = nullptr;
+  int alternate = 0;  // whole-range applies alternate their sweep direction (hf_tangent_set_alternate)
+  int flip = 0;
 };
 
 struct hf_transfer {
@@ -507,6 +509,10 @@ static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, con
   a.skip = skip_dev;
   a.fill = fill;
   a.reserve_sms = reserve_sms;
+  if (op->alternate && tile1 < 0) {  // whole-range apply: every other sweep backwards
+    a.reverse = op->flip;
+    op->flip ^= 1;
+  }
   HF_CUDA(cell(op->sp, OP_APPLY, op->strategy, a, S(stream)));
   return HF_OK;
 }
@@ -568,6 +574,13 @@ HF_API int hf_tangent_apply_tiles_ex(hf_tangent* op, const double* x_dev, double
     return fail(HF_ERR_ARG, "bad tile range, mode or reserve");
   if (!op || op->sp->lat.n_el == 0 || tile1 == tile0) return op ? HF_OK : fail(HF_ERR_ARG, "null tangent");
   return tangent_apply(op, x_dev, y_dev, skip_dev, mode, stream, tile0, tile1, reserve_sms);
+}
+
+HF_API int hf_tangent_set_alternate(hf_tangent* op, int on) {
+  if (!op) return fail(HF_ERR_ARG, "null tangent");
+  op->alternate = on != 0;
+  op->flip = 0;
+  return HF_OK;
 }
 
 HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream) {

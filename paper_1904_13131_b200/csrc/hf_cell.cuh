@@ -74,6 +74,7 @@ struct CellArgs {
   long long cache_len;      // cache elements (bounds checks of the debug build)
   long long tile0, tile1;   // apply: tile range; tile1 < 0 means all tiles
   int reserve_sms = 0;      // apply: leave this many SMs' worth of blocks free (a concurrent NCCL kernel)
+  int reverse = 0;          // apply: walk the tile range backwards
   unsigned long long* detmin;  // ordered-double min of det F (build / residual / range)
   unsigned long long* detmax;
 };

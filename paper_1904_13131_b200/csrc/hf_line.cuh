@@ -73,6 +73,7 @@ struct LineArgs {
   // 2: PDL secondary of a kernel that wrote x and y (hf_cheb_step_fill): wait before the first gather
   int fill;
   long long tile0, tile1;  // tile range of this launch (interior/boundary split of a slab)
+  int reverse;             // walk the tile range backwards (alternating sweeps reuse L2, hf_tangent_set_alternate)
   long long cache_len;     // cache elements (bounds checks of the debug build)
 };
 
@@ -478,9 +479,12 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(lbuf + (size_t)W * NB * Y::BUF) + warp * RW;
   const long long ntiles = a.tile1;  // tiles [a.tile0, a.tile1) of the (CPW-cell) tiling
   const long long tstride = (long long)N * CH;
+  // the tile whose data a work slot processes: the range walked forwards, or
+  // backwards when a.reverse (slots past the range stay past it)
+  auto dtile = [&](long long tl) { return (a.reverse && tl < a.tile1) ? a.tile1 - 1 - (tl - a.tile0) : tl; };
   // chunk j of this warp: tile tile0 + blockIdx.x + (warp + (j / N) * W) * gridDim.x, iq = j % N
   auto issue = [&](long long j) {
-    const long long tile = a.tile0 + blockIdx.x + (warp + (j / N) * W) * (long long)gridDim.x;
+    const long long tile = dtile(a.tile0 + blockIdx.x + (warp + (j / N) * W) * (long long)gridDim.x);
     if (tile >= ntiles) return;
     const int s = (int)(j % RW);
     HF_ASSERT(tile * tstride + (j % N + 1) * CH <= a.cache_len);
@@ -514,10 +518,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   long long jc = 0;  // this warp's chunk counter
   const long long tstep = (long long)W * gridDim.x;
   Gather<DIM, N, VAR> nxt;
-  gather_tile<DIM, N, VAR, ST>(a, a.tile0 + blockIdx.x + (long long)warp * gridDim.x, ntiles, m, t, act, nxt);
+  gather_tile<DIM, N, VAR, ST>(a, dtile(a.tile0 + blockIdx.x + (long long)warp * gridDim.x), ntiles, m, t, act, nxt);
   for (long long tile = a.tile0 + blockIdx.x + (long long)warp * gridDim.x; tile < ntiles; tile += tstep) {
     const Gather<DIM, N, VAR> g = nxt;
-    gather_tile<DIM, N, VAR, ST>(a, tile + tstep, ntiles, m, t, act, nxt);  // in flight during this tile
+    gather_tile<DIM, N, VAR, ST>(a, dtile(tile + tstep), ntiles, m, t, act, nxt);  // in flight during this tile
     const long long e = g.e;
     const bool live = g.live;
     double u[DIM][N];
