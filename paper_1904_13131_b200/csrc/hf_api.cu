@@ -41,6 +41,14 @@ inline unsigned vec_blocks(long long n) {
   return (unsigned)b;
 }
 
+// the fill: four elements per thread per iteration, one resident wave (148 SMs x 8 blocks of 256)
+inline unsigned fill_blocks(long long n) {
+  long long b = (n + 1023) / 1024;
+  if (b < 1) b = 1;
+  if (b > 148 * 8) b = 148 * 8;
+  return (unsigned)b;
+}
+
 // Gauss-Jordan inverse of a small dense matrix (row-major), returns false if singular
 bool invert(std::vector<double> a, int n, std::vector<double>& inv) {
   inv.assign(n * n, 0.0);
@@ -533,10 +541,10 @@ HF_API int hf_tangent_apply_flagged(hf_tangent* op, const double* x_dev, double*
     pdl = e ? std::atoi(e) : 1;
   }
   if (op->fp32)
-    k_fill_masked<float><<<vec_blocks(op->sp->n_dofs), 256, 0, S(stream)>>>(
+    k_fill_masked<float><<<fill_blocks(op->sp->n_dofs), 256, 0, S(stream)>>>(
         op->sp->n_dofs, (float*)y_dev, (const float*)x_dev, op->sp->d_mask, 0.0, skip_dev);
   else
-    k_fill_masked<<<vec_blocks(op->sp->n_dofs), 256, 0, S(stream)>>>(op->sp->n_dofs, y_dev, x_dev, op->sp->d_mask,
+    k_fill_masked<<<fill_blocks(op->sp->n_dofs), 256, 0, S(stream)>>>(op->sp->n_dofs, y_dev, x_dev, op->sp->d_mask,
                                                                      0.0, skip_dev);
   HF_CUDA(cudaGetLastError());
   if (op->sp->lat.n_el == 0) return HF_OK;
@@ -678,7 +686,7 @@ static int host_pipe_enqueue(hf_tangent* op, HostPipe* h, const double* xh, doub
     int mode = 0;
     if (hi > filled) {
       const long long off = filled * plane, cnt = (hi - filled) * plane;
-      k_fill_masked<double><<<vec_blocks(cnt), 256, 0, h->cap>>>(cnt, h->yd + off, h->xd + off, sp->d_mask + off, 0.0,
+      k_fill_masked<double><<<fill_blocks(cnt), 256, 0, h->cap>>>(cnt, h->yd + off, h->xd + off, sp->d_mask + off, 0.0,
                                                                  nullptr);
       HF_CUDA(cudaGetLastError());
       filled = hi;
@@ -876,7 +884,7 @@ HF_API int hf_tangent_diagonal(hf_tangent* op, double* d_dev, void* stream) {
   if (op->fp32) return fail(HF_ERR_UNSUPPORTED, "diagonal of an fp32-storage tangent: use the fp64 operator");
   const hf_space* sp = op->sp;
   cudaStream_t s = S(stream);
-  k_fill_masked<double><<<vec_blocks(sp->n_dofs), 256, 0, s>>>(sp->n_dofs, d_dev, nullptr, sp->d_mask, 1.0, nullptr);
+  k_fill_masked<double><<<fill_blocks(sp->n_dofs), 256, 0, s>>>(sp->n_dofs, d_dev, nullptr, sp->d_mask, 1.0, nullptr);
   HF_CUDA(cudaGetLastError());
   CellArgs a = base_args(sp);
   a.y = d_dev;
@@ -1089,7 +1097,7 @@ HF_API int hf_dot(hf_ws* w, long long n, const double* a, const double* b, doubl
 HF_API int hf_fill_masked(long long n, double* y, const double* x, const unsigned char* mask, double masked_value,
                           void* stream) {
   if (!y || !mask) return fail(HF_ERR_ARG, "null argument");
-  k_fill_masked<<<vec_blocks(n), 256, 0, S(stream)>>>(n, y, x, mask, masked_value, nullptr);
+  k_fill_masked<<<fill_blocks(n), 256, 0, S(stream)>>>(n, y, x, mask, masked_value, nullptr);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }
@@ -1105,7 +1113,7 @@ HF_API int hf_probe_dfma(long long iters, int blocks, int threads, double* sink_
 HF_API int hf_fill_masked_f32(long long n, float* y, const float* x, const unsigned char* mask, double masked_value,
                               void* stream) {
   if (!y || !mask) return fail(HF_ERR_ARG, "null argument");
-  k_fill_masked<float><<<vec_blocks(n), 256, 0, S(stream)>>>(n, y, x, mask, masked_value, nullptr);
+  k_fill_masked<float><<<fill_blocks(n), 256, 0, S(stream)>>>(n, y, x, mask, masked_value, nullptr);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }

@@ -96,8 +96,25 @@ __global__ void k_fill_masked(long long n, T* __restrict__ y, const T* __restric
                               const uint8_t* __restrict__ mask, double mval, const int* skip) {
   asm volatile("griddepcontrol.launch_dependents;");  // a PDL secondary (the apply) may start now
   if (skip && *skip) return;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    y[i] = mask[i] ? (x ? x[i] : (T)mval) : (T)0;
+  // four elements per thread and iteration, every load issued before any use
+  // (x is read whether or not the mask selects it: no load behind a branch)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    uint8_t m[4];
+    T v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      m[k] = mask[i + k * stride];
+      v[k] = x ? x[i + k * stride] : (T)mval;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y[i + k * stride] = m[k] ? v[k] : (T)0;
+  }
+  for (; i < n; i += stride) {
+    const T v = x ? x[i] : (T)mval;
+    y[i] = mask[i] ? v : (T)0;
+  }
 }
 
 // Chebyshev step (multigrid.py:176-205, 280-296):
