@@ -65,6 +65,17 @@ HF_API const char* hf_last_error(void);
 HF_API int hf_abi_version(void);
 HF_API int hf_max_degree(int dim);
 
+/* ---- Device block pool (no reference analogue: numpy allocates per call).
+ * Every device allocation of the library is pooled: a freed block is kept
+ * (after a device synchronisation, the ordering cudaFree gives) and reused
+ * for a later request of the same size, so rebuilding the tangent and GMG
+ * hierarchy each Newton iteration (solver.py:174) does not go back to the
+ * driver.  HF_POOL_MAX_MB caps the pooled bytes (default 32768).
+ * hf_pool_release returns every pooled block to the driver; hf_pool_info
+ * reports pooled (free) and live (handed-out) bytes. */
+HF_API int hf_pool_release(void);
+HF_API int hf_pool_info(long long* pooled_bytes, long long* live_bytes);
+
 /* ---- Problem (operators.py:83-116; build_dof_map fespace.py:125-139;
  *      compute_geometry_cache mesh.py:290-307) -------------------------------
  * cells[dim] per-axis cell counts of a structured box lattice (the reference

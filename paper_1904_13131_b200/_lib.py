@@ -36,6 +36,8 @@ _SIGS = {
     "hf_last_error": (ct.c_char_p, []),
     "hf_abi_version": (I, []),
     "hf_max_degree": (I, [I]),
+    "hf_pool_release": (I, []),
+    "hf_pool_info": (I, [P, P]),
     "hf_space_create": (I, [I, I, I, P, P, P, P, P, P, P, P, P, P, ct.POINTER(P)]),
     "hf_space_set_mask": (I, [P, P, P]),
     "hf_space_info": (I, [P, ct.POINTER(LL), ct.POINTER(LL), ct.POINTER(LL)]),

@@ -8,7 +8,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/hf.h"
@@ -33,6 +36,91 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// Device block pool.  Every device allocation of this library goes through
+// dmalloc/dfree.  A Newton iteration rebuilds the tangent and the whole GMG
+// hierarchy (solver.py:174, multigrid.py:358-369) with the same sizes as the
+// previous one; returning blocks to cudaFree and asking cudaMalloc again costs
+// tens of ms per iteration at 64^3 (page unmapping/mapping of GB-sized caches).
+// Freed blocks are kept per device and handed out again for requests of the
+// same size (within +12.5 %).  dfree synchronises the device before pooling a
+// block, the same ordering guarantee cudaFree gives, so no queued kernel still
+// reads a block when it is reused.  Pooled bytes are capped (HF_POOL_MAX_MB,
+// default 32768); hf_pool_release() returns every pooled block to the driver,
+// and an allocation that fails releases the pool and retries once.
+struct DevPool {
+  std::mutex m;
+  std::multimap<std::pair<int, size_t>, void*> free_blocks;
+  std::unordered_map<void*, std::pair<int, size_t>> owned;
+  size_t pooled = 0, live = 0, cap = 0;
+  DevPool() {
+    const char* e = std::getenv("HF_POOL_MAX_MB");
+    cap = (size_t)(e ? std::atoll(e) : 32768) << 20;
+  }
+  void release_locked() {
+    for (auto& kv : free_blocks) {
+      cudaFree(kv.second);
+      owned.erase(kv.second);
+    }
+    free_blocks.clear();
+    pooled = 0;
+  }
+};
+
+DevPool& dev_pool() {
+  static DevPool* p = new DevPool();  // never destroyed: outlives static teardown order
+  return *p;
+}
+
+cudaError_t dmalloc(void** ptr, size_t bytes) {
+  DevPool& P = dev_pool();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (bytes == 0) bytes = 1;
+  std::lock_guard<std::mutex> g(P.m);
+  auto it = P.free_blocks.lower_bound({dev, bytes});
+  if (it != P.free_blocks.end() && it->first.first == dev && it->first.second <= bytes + bytes / 8) {
+    *ptr = it->second;
+    P.pooled -= it->first.second;
+    P.live += it->first.second;
+    P.free_blocks.erase(it);
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaErrorMemoryAllocation && !P.free_blocks.empty()) {
+    cudaGetLastError();
+    P.release_locked();
+    e = cudaMalloc(ptr, bytes);
+  }
+  if (e == cudaSuccess) {
+    P.owned[*ptr] = {dev, bytes};
+    P.live += bytes;
+  }
+  return e;
+}
+
+cudaError_t dfree(void* ptr) {
+  if (!ptr) return cudaSuccess;
+  DevPool& P = dev_pool();
+  std::lock_guard<std::mutex> g(P.m);
+  auto it = P.owned.find(ptr);
+  if (it == P.owned.end()) return cudaFree(ptr);
+  const auto key = it->second;
+  P.live -= key.second;
+  if (P.pooled + key.second > P.cap) {
+    P.owned.erase(it);
+    return cudaFree(ptr);
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != key.first) cudaSetDevice(key.first);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (cur != key.first) cudaSetDevice(cur);
+  P.free_blocks.emplace(key, ptr);
+  P.pooled += key.second;
+  return e;
+}
 
 inline unsigned vec_blocks(long long n) {
   long long b = (n + 255) / 256;
@@ -230,6 +318,21 @@ extern "C" {
 HF_API const char* hf_last_error(void) { return g_err.c_str(); }
 HF_API int hf_abi_version(void) { return HF_ABI_VERSION; }
 
+HF_API int hf_pool_release(void) {
+  DevPool& P = dev_pool();
+  std::lock_guard<std::mutex> g(P.m);
+  P.release_locked();
+  return HF_OK;
+}
+
+HF_API int hf_pool_info(long long* pooled_bytes, long long* live_bytes) {
+  DevPool& P = dev_pool();
+  std::lock_guard<std::mutex> g(P.m);
+  if (pooled_bytes) *pooled_bytes = (long long)P.pooled;
+  if (live_bytes) *live_bytes = (long long)P.live;
+  return HF_OK;
+}
+
 HF_API int hf_max_degree(int dim) { return dim == 2 ? 8 : (dim == 3 ? 4 : 0); }
 
 // ---------------------------------------------------------------------------
@@ -301,7 +404,7 @@ HF_API int hf_space_create(int dim, int degree, int nq1, const int* cells, const
   long long nverts = 1;
   for (int a = 0; a < dim; ++a) nverts *= (cells[a] + 1);
   double* d_verts = nullptr;
-#define ALLOC(ptr, bytes) HF_CUDA(cudaMalloc((void**)&(ptr), (bytes)))
+#define ALLOC(ptr, bytes) HF_CUDA(dmalloc((void**)&(ptr), (bytes)))
   ALLOC(sp->d_jinv, sizeof(double) * dim * dim * sp->lat.n_qp);
   ALLOC(sp->d_jxw, sizeof(double) * sp->lat.n_qp);
   ALLOC(sp->d_mu, sizeof(double) * nel);
@@ -321,7 +424,7 @@ HF_API int hf_space_create(int dim, int degree, int nq1, const int* cells, const
   unsigned long long o = 0;
   HF_CUDA(cudaMemcpyAsync(&o, sp->d_u64, sizeof(o), cudaMemcpyDeviceToHost, s));
   HF_CUDA(cudaStreamSynchronize(s));
-  cudaFree(d_verts);
+  dfree(d_verts);
   if (nel > 0 && !(hf_unord(o) > 0.0)) {
     hf_space_destroy(sp);
     char buf[128];
@@ -368,13 +471,13 @@ HF_API int hf_space_geometry_copy(const hf_space* sp, double* jinv_dev, double* 
 
 HF_API int hf_space_destroy(hf_space* sp) {
   if (!sp) return HF_OK;
-  cudaFree(sp->d_jinv);
-  cudaFree(sp->d_jxw);
-  cudaFree(sp->d_mu);
-  cudaFree(sp->d_lam);
-  cudaFree(sp->d_mask);
-  cudaFree(sp->d_lmask);
-  cudaFree(sp->d_u64);
+  dfree(sp->d_jinv);
+  dfree(sp->d_jxw);
+  dfree(sp->d_mu);
+  dfree(sp->d_lam);
+  dfree(sp->d_mask);
+  dfree(sp->d_lmask);
+  dfree(sp->d_u64);
   delete sp;
   return HF_OK;
 }
@@ -472,9 +575,9 @@ HF_API int hf_tangent_create_ex(hf_space* sp, int strategy, int storage_bits, co
   const int esz = op->fp32 ? 4 : 8;
   const long long ncache = tile_cache_doubles(sp->dim, sp->n1, op->nf, sp->lat.n_el, esz);
   op->cache_len = ncache;
-  HF_CUDA(cudaMalloc((void**)&op->d_cache, (size_t)esz * (ncache > 0 ? ncache : 1)));
+  HF_CUDA(dmalloc((void**)&op->d_cache, (size_t)esz * (ncache > 0 ? ncache : 1)));
   if (strategy == HF_SCALAR) {
-    HF_CUDA(cudaMalloc((void**)&op->d_ubar, sizeof(double) * sp->n_dofs));
+    HF_CUDA(dmalloc((void**)&op->d_ubar, sizeof(double) * sp->n_dofs));
     HF_CUDA(cudaMemcpyAsync(op->d_ubar, ubar_dev, sizeof(double) * sp->n_dofs, cudaMemcpyDeviceToDevice, s));
   }
   unsigned long long init = ~0ull;
@@ -604,8 +707,8 @@ static void host_pipe_free(HostPipe* h) {
   if (h->cap) cudaStreamDestroy(h->cap);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
-  cudaFree(h->xd);
-  cudaFree(h->yd);
+  dfree(h->xd);
+  dfree(h->yd);
   delete h;
 }
 
@@ -752,8 +855,8 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
   HostPipe* h = op->host;
   if (!h) {
     h = op->host = new HostPipe();
-    HF_CUDA(cudaMalloc((void**)&h->xd, bytes));
-    HF_CUDA(cudaMalloc((void**)&h->yd, bytes));
+    HF_CUDA(dmalloc((void**)&h->xd, bytes));
+    HF_CUDA(dmalloc((void**)&h->yd, bytes));
     HF_CUDA(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
     HF_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
     HF_CUDA(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
@@ -911,8 +1014,8 @@ HF_API int hf_tangent_storage(const hf_tangent* op, long long* storage_bytes, in
 HF_API int hf_tangent_destroy(hf_tangent* op) {
   if (!op) return HF_OK;
   host_pipe_free(op->host);
-  cudaFree(op->d_cache);
-  cudaFree(op->d_ubar);
+  dfree(op->d_cache);
+  dfree(op->d_ubar);
   delete op;
   return HF_OK;
 }
@@ -996,12 +1099,12 @@ HF_API int hf_transfer_create(const hf_space* coarse, const hf_space* fine, cons
         }
       rp.push_back((int)rc.size());
     }
-    HF_CUDA(cudaMalloc((void**)&t->d_pp[a], sizeof(int) * pp.size()));
-    HF_CUDA(cudaMalloc((void**)&t->d_pc[a], sizeof(int) * (pc.size() + 1)));
-    HF_CUDA(cudaMalloc((void**)&t->d_pw[a], sizeof(double) * (pw.size() + 1)));
-    HF_CUDA(cudaMalloc((void**)&t->d_rp[a], sizeof(int) * rp.size()));
-    HF_CUDA(cudaMalloc((void**)&t->d_rc[a], sizeof(int) * (rc.size() + 1)));
-    HF_CUDA(cudaMalloc((void**)&t->d_rw[a], sizeof(double) * (rw.size() + 1)));
+    HF_CUDA(dmalloc((void**)&t->d_pp[a], sizeof(int) * pp.size()));
+    HF_CUDA(dmalloc((void**)&t->d_pc[a], sizeof(int) * (pc.size() + 1)));
+    HF_CUDA(dmalloc((void**)&t->d_pw[a], sizeof(double) * (pw.size() + 1)));
+    HF_CUDA(dmalloc((void**)&t->d_rp[a], sizeof(int) * rp.size()));
+    HF_CUDA(dmalloc((void**)&t->d_rc[a], sizeof(int) * (rc.size() + 1)));
+    HF_CUDA(dmalloc((void**)&t->d_rw[a], sizeof(double) * (rw.size() + 1)));
     HF_CUDA(cudaMemcpy(t->d_pp[a], pp.data(), sizeof(int) * pp.size(), cudaMemcpyHostToDevice));
     HF_CUDA(cudaMemcpy(t->d_pc[a], pc.data(), sizeof(int) * pc.size(), cudaMemcpyHostToDevice));
     HF_CUDA(cudaMemcpy(t->d_pw[a], pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice));
@@ -1011,8 +1114,8 @@ HF_API int hf_transfer_create(const hf_space* coarse, const hf_space* fine, cons
   }
   // largest intermediate: fine nodes (all passes are bounded by the fine lattice)
   t->tmp_len = fine->n_dofs;
-  HF_CUDA(cudaMalloc((void**)&t->d_tmp[0], sizeof(double) * t->tmp_len));
-  HF_CUDA(cudaMalloc((void**)&t->d_tmp[1], sizeof(double) * t->tmp_len));
+  HF_CUDA(dmalloc((void**)&t->d_tmp[0], sizeof(double) * t->tmp_len));
+  HF_CUDA(dmalloc((void**)&t->d_tmp[1], sizeof(double) * t->tmp_len));
   *out = t;
   return HF_OK;
 }
@@ -1041,15 +1144,15 @@ HF_API int hf_restrict_ex(hf_transfer* t, const void* rf, int in_bits, void* rc,
 HF_API int hf_transfer_destroy(hf_transfer* t) {
   if (!t) return HF_OK;
   for (int a = 0; a < 3; ++a) {
-    cudaFree(t->d_pp[a]);
-    cudaFree(t->d_pc[a]);
-    cudaFree(t->d_pw[a]);
-    cudaFree(t->d_rp[a]);
-    cudaFree(t->d_rc[a]);
-    cudaFree(t->d_rw[a]);
+    dfree(t->d_pp[a]);
+    dfree(t->d_pc[a]);
+    dfree(t->d_pw[a]);
+    dfree(t->d_rp[a]);
+    dfree(t->d_rc[a]);
+    dfree(t->d_rw[a]);
   }
-  cudaFree(t->d_tmp[0]);
-  cudaFree(t->d_tmp[1]);
+  dfree(t->d_tmp[0]);
+  dfree(t->d_tmp[1]);
   delete t;
   return HF_OK;
 }
@@ -1071,8 +1174,8 @@ HF_API int hf_inject(const hf_space* coarse, const hf_space* fine, const double*
 HF_API int hf_ws_create(hf_ws** out) {
   if (!out) return fail(HF_ERR_ARG, "null argument");
   hf_ws* w = new hf_ws();
-  HF_CUDA(cudaMalloc((void**)&w->d_partials, sizeof(double) * RED_MAX_BLOCKS));
-  HF_CUDA(cudaMalloc((void**)&w->d_counter, sizeof(unsigned)));
+  HF_CUDA(dmalloc((void**)&w->d_partials, sizeof(double) * RED_MAX_BLOCKS));
+  HF_CUDA(dmalloc((void**)&w->d_counter, sizeof(unsigned)));
   HF_CUDA(cudaMemset(w->d_counter, 0, sizeof(unsigned)));
   *out = w;
   return HF_OK;
@@ -1080,8 +1183,8 @@ HF_API int hf_ws_create(hf_ws** out) {
 
 HF_API int hf_ws_destroy(hf_ws* w) {
   if (!w) return HF_OK;
-  cudaFree(w->d_partials);
-  cudaFree(w->d_counter);
+  dfree(w->d_partials);
+  dfree(w->d_counter);
   delete w;
   return HF_OK;
 }
@@ -1292,10 +1395,10 @@ static int coarse_build(long long n, long long nnz, const std::vector<int>& rp, 
   c->grid = grid;
   c->smem = smem;
   c->blob_bytes = blob.size();
-  HF_CUDA(cudaMalloc((void**)&c->blob, blob.size()));
-  HF_CUDA(cudaMalloc((void**)&c->boff, sizeof(long long) * grid));
-  HF_CUDA(cudaMalloc((void**)&c->xb, sizeof(double) * n));
-  HF_CUDA(cudaMalloc((void**)&c->partials, sizeof(double) * grid));
+  HF_CUDA(dmalloc((void**)&c->blob, blob.size()));
+  HF_CUDA(dmalloc((void**)&c->boff, sizeof(long long) * grid));
+  HF_CUDA(dmalloc((void**)&c->xb, sizeof(double) * n));
+  HF_CUDA(dmalloc((void**)&c->partials, sizeof(double) * grid));
   HF_CUDA(cudaMemcpyAsync(c->blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, s));
   HF_CUDA(cudaMemcpyAsync(c->boff, boff.data(), sizeof(long long) * grid, cudaMemcpyHostToDevice, s));
   HF_CUDA(cudaStreamSynchronize(s));
@@ -1335,7 +1438,7 @@ HF_API int hf_coarse_create_space(const hf_space* sp, void* stream, hf_coarse** 
   const int nld = nloc * sp->dim;
   if (n >= (1ll << 31) || nel * nld * nld >= (1ll << 31)) return fail(HF_ERR_UNSUPPORTED, "coarse level too large");
   long long* d_dofs = nullptr;
-  HF_CUDA(cudaMalloc((void**)&d_dofs, sizeof(long long) * std::max(1ll, nel * nld)));
+  HF_CUDA(dmalloc((void**)&d_dofs, sizeof(long long) * std::max(1ll, nel * nld)));
   std::vector<long long> dofs(nel * nld);
   std::vector<unsigned char> mask(n);
   cudaError_t e = launch_cell_dofs(sp->lat, sp->dim, sp->degree, d_dofs, s);
@@ -1343,7 +1446,7 @@ HF_API int hf_coarse_create_space(const hf_space* sp, void* stream, hf_coarse** 
     e = cudaMemcpyAsync(dofs.data(), d_dofs, sizeof(long long) * nel * nld, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(mask.data(), sp->d_mask, n, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(d_dofs);
+  dfree(d_dofs);
   HF_CUDA(e);
   struct Ent {
     int r, c, k;  // k = element-matrix entry, -1 = unit diagonal of a constrained row
@@ -1392,10 +1495,10 @@ HF_API int hf_coarse_create_space(const hf_space* sp, void* stream, hf_coarse** 
   c->nupd = (int)slot_of_upd.size();
   std::vector<long long> uoff(c->nupd);
   for (int u = 0; u < c->nupd; ++u) uoff[u] = slot_off[slot_of_upd[u]];
-  HF_CUDA(cudaMalloc((void**)&c->cptr, sizeof(int) * (c->nupd + 1)));
-  HF_CUDA(cudaMalloc((void**)&c->cidx, sizeof(int) * std::max<size_t>(1, cidx.size())));
-  HF_CUDA(cudaMalloc((void**)&c->uoff, sizeof(long long) * std::max(1, c->nupd)));
-  HF_CUDA(cudaMalloc((void**)&c->elem, sizeof(double) * std::max(1ll, nel * nld * nld)));
+  HF_CUDA(dmalloc((void**)&c->cptr, sizeof(int) * (c->nupd + 1)));
+  HF_CUDA(dmalloc((void**)&c->cidx, sizeof(int) * std::max<size_t>(1, cidx.size())));
+  HF_CUDA(dmalloc((void**)&c->uoff, sizeof(long long) * std::max(1, c->nupd)));
+  HF_CUDA(dmalloc((void**)&c->elem, sizeof(double) * std::max(1ll, nel * nld * nld)));
   HF_CUDA(cudaMemcpyAsync(c->cptr, cptr.data(), sizeof(int) * (c->nupd + 1), cudaMemcpyHostToDevice, s));
   if (!cidx.empty())
     HF_CUDA(cudaMemcpyAsync(c->cidx, cidx.data(), sizeof(int) * cidx.size(), cudaMemcpyHostToDevice, s));
@@ -1436,7 +1539,7 @@ HF_API int hf_coarse_clone(const hf_coarse* src, void* stream, hf_coarse** out) 
   c->uoff = nullptr;
   c->elem = nullptr;
   auto dup = [&](void** dst, const void* from, size_t bytes) -> cudaError_t {
-    cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 8));
+    cudaError_t e = dmalloc(dst, std::max<size_t>(bytes, 8));
     if (e == cudaSuccess && from && bytes) e = cudaMemcpyAsync(*dst, from, bytes, cudaMemcpyDeviceToDevice, s);
     return e;
   };
@@ -1468,14 +1571,14 @@ HF_API int hf_coarse_clone(const hf_coarse* src, void* stream, hf_coarse** out) 
 
 HF_API int hf_coarse_destroy(hf_coarse* c) {
   if (!c) return HF_OK;
-  cudaFree(c->blob);
-  cudaFree(c->boff);
-  cudaFree(c->xb);
-  cudaFree(c->partials);
-  cudaFree(c->cptr);
-  cudaFree(c->cidx);
-  cudaFree(c->uoff);
-  cudaFree(c->elem);
+  dfree(c->blob);
+  dfree(c->boff);
+  dfree(c->xb);
+  dfree(c->partials);
+  dfree(c->cptr);
+  dfree(c->cidx);
+  dfree(c->uoff);
+  dfree(c->elem);
   delete c;
   return HF_OK;
 }

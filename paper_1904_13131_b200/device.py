@@ -73,3 +73,25 @@ class Workspace:
 def dot(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, skip=None) -> torch.Tensor:
     check(lib().hf_dot(Workspace.get().handle, a.numel(), ptr(a), ptr(b), ptr(out), ptr(skip), stream()))
     return out
+
+
+def capture_graph(fn) -> torch.cuda.CUDAGraph:
+    """Capture ``fn``'s launches into a CUDA graph on a side stream.
+
+    ``torch.cuda.graph`` empties the caching allocator on entry; a Newton
+    iteration captures a fresh V-cycle graph for every rebuilt hierarchy, and
+    emptying the cache each time sent every later allocation back to
+    cudaMalloc.  Capturing with ``capture_begin/capture_end`` directly keeps
+    the cache."""
+    g = torch.cuda.CUDAGraph()
+    cur = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        g.capture_begin()
+        try:
+            fn()
+        finally:
+            g.capture_end()
+    cur.wait_stream(side)
+    return g

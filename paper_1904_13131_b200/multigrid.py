@@ -518,10 +518,7 @@ class GMGPreconditioner:
         else:
             if self._graph is None:
                 self._run()  # eager warm-up, then capture the identical launch sequence
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._run()
-                self._graph = g
+                self._graph = dv.capture_graph(self._run)
                 self._b.copy_(b)
             self._graph.replay()
         out.copy_(self._x)

@@ -45,3 +45,11 @@ def test_product_path_fails_loudly_without_cuda(monkeypatch):
         pytest.skip("has a GPU")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         device.require_cuda()
+
+
+def test_pool_info_without_a_device():
+    L = _lib.lib()
+    pooled, live = ct.c_longlong(-1), ct.c_longlong(-1)
+    assert L.hf_pool_release() == 0
+    assert L.hf_pool_info(ct.byref(pooled), ct.byref(live)) == 0
+    assert pooled.value == 0 and live.value >= 0

@@ -160,3 +160,32 @@ def test_residual_is_energy_gradient(name, lib_loaded):
     fd = (energy(p, g["ubar"] + eps * v, g["traction"]) - energy(p, g["ubar"] - eps * v, g["traction"])) / (2 * eps)
     r = compute_residual(p, g["ubar"], g["traction"])
     assert abs(fd - r @ v) <= 1e-6 * max(1.0, abs(r @ v))
+
+
+def test_device_pool_reuses_freed_blocks(lib_loaded):
+    """A rebuilt tangent takes its cache from the pool (hf_pool_*), and the
+    reused (stale) block gives the same bits as a fresh one."""
+    import ctypes as ct
+
+    from paper_1904_13131_b200 import MatrixFreeTangent
+
+    L = lib_loaded
+    g = golden(CASES[0])
+    p = product_problem(g)
+
+    def info():
+        pooled, live = ct.c_longlong(), ct.c_longlong()
+        assert L.hf_pool_info(ct.byref(pooled), ct.byref(live)) == 0
+        return pooled.value, live.value
+
+    assert L.hf_pool_release() == 0
+    y0 = MatrixFreeTangent(p, g["ubar"], "tensor4").apply(g["x"])  # built, applied, destroyed
+    pooled, live = info()
+    assert pooled > 0
+    op = MatrixFreeTangent(p, g["ubar"], "tensor4")
+    pooled2, live2 = info()
+    assert pooled2 < pooled and live2 > live
+    assert np.array_equal(op.apply(g["x"]), y0)
+    del op
+    assert L.hf_pool_release() == 0
+    assert info()[0] == 0

@@ -1,6 +1,6 @@
 """Kernel-time breakdown of GMG-preconditioned CG iterations (torch.profiler / CUPTI).
 
-    python tools/prof_cg.py [cfg=4] [iterations=5]
+    python tools/prof_cg.py [cfg=4] [iterations=5] [strategy=tensor4]
 
 Builds the config's GMG hierarchy at the first Newton iterate of load step 1
 (cfg 4) or at the synthetic SPD state (others), warms up, then profiles
@@ -20,6 +20,7 @@ from paper_1904_13131_b200.workloads import AMP_SOLVE, make_workload  # noqa: E4
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 its = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+strategy = sys.argv[3] if len(sys.argv) > 3 else "tensor4"
 wl = make_workload(cfg, seed=0, levels=True, amp=AMP_SOLVE, with_x=(cfg != 4))
 probs = wl.problems
 fine = probs[-1]
@@ -34,8 +35,8 @@ else:
     b = MatrixFreeTangent(fine, u, "tensor4").apply(torch.from_numpy(wl.x).cuda())
     b[fine.mask_dev] = 0.0
     keep = False
-op = MatrixFreeTangent(fine, u, "tensor4")
-gmg = build_gmg(probs, u, "tensor4", seed=0, keep_constrained=keep, coarse_precision=os.environ.get("HF_COARSE_PRECISION", "fp64"))
+op = MatrixFreeTangent(fine, u, strategy)
+gmg = build_gmg(probs, u, strategy, seed=0, keep_constrained=keep, coarse_precision=os.environ.get("HF_COARSE_PRECISION", "fp64"))
 cg(op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=2)  # warm-up + graph capture
 torch.cuda.synchronize()
 t0 = time.perf_counter()
@@ -56,7 +57,7 @@ for e in prof.events():
     a[0] += 1
     a[1] += e.device_time
 tot = sum(v[1] for v in agg.values())
-print(json.dumps({"cfg": cfg, "levels": [p.mesh.cells[0] for p in probs], "iterations": its,
+print(json.dumps({"cfg": cfg, "strategy": strategy, "levels": [p.mesh.cells[0] for p in probs], "iterations": its,
                   "wall_ms_per_iteration": wall / its * 1e3, "kernel_ms_per_iteration": tot / its / 1e3}))
 for n, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:25]:
     print(json.dumps({"kernel": n, "count_per_it": c / its, "ms_per_it": t / its / 1e3, "share": t / tot}))
