@@ -266,7 +266,11 @@ HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, cons
  * max_applications - 1 further applications with the residual test
  * ||b - A x|| <= rel_target ||b|| every `degree`-th application; scal_dev[0..2]
  * = ||b||^2, target, last ||b - A x||^2; *flag_dev = 1 if it stopped on the
- * test (or b == 0), 0 if it hit the cap.  d is scratch.  Graph-capturable. */
+ * test (or b == 0), 0 if it hit the cap.  d is scratch.  Graph-capturable.
+ * A level whose whole matrix and iterate fit one CTA's shared memory runs as
+ * a single CTA without grid barriers (HF_COARSE_SINGLE=0 forces the
+ * multi-CTA form); the result differs only in the summation order of the
+ * residual norm. */
 HF_API int hf_coarse_create(long long n, long long nnz, const int* rowptr_dev, const int* col_dev,
                             const double* val_dev, void* stream, hf_coarse** out);
 HF_API int hf_coarse_cheb_solve(hf_coarse* c, const double* b, double* x, double* d, const double* inv_d,

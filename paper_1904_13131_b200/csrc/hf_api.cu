@@ -1346,8 +1346,14 @@ static int coarse_build(long long n, long long nnz, const std::vector<int>& rp, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   // one CTA per SM (the grid barrier costs the same ~1.2 us from 35 to 148
-  // CTAs on B200, tools/probes/gridsync_probe.cu), fewer for tiny levels
-  const int grid = (int)std::max(1ll, std::min<long long>(nsm, (n + 7) / 8));
+  // CTAs on B200, tools/probes/gridsync_probe.cu), fewer for tiny levels; a
+  // level whose whole block (values, columns, rows, iterate) fits one CTA's
+  // shared memory runs as a single CTA without grid barriers
+  const size_t one_cta = coarse_align16(8ull * nnz) + coarse_align16(4ull * n) + coarse_align16(4ull * (n + 1)) +
+                         coarse_align16(2ull * nnz) + 8ull * 6 * n;
+  const char* single_env = std::getenv("HF_COARSE_SINGLE");  // "0": always the multi-CTA form (tests)
+  const bool single = one_cta <= 160 * 1024 && n <= 65535 && !(single_env && single_env[0] == '0');
+  const int grid = single ? 1 : (int)std::max(1ll, std::min<long long>(nsm, (n + 7) / 8));
   const int rows_per = (int)((n + grid - 1) / grid);
   std::vector<unsigned char> blob;
   std::vector<long long> boff(grid);
@@ -1365,7 +1371,7 @@ static int coarse_build(long long n, long long nnz, const std::vector<int>& rp, 
     for (size_t q = 0; q < u.size(); ++q) pos[u[q]] = (int)q;
     const size_t body = coarse_align16(8ull * nz) + coarse_align16(4ull * u.size()) +
                         coarse_align16(4ull * (rows + 1)) + coarse_align16(2ull * nz);
-    smem = std::max<size_t>(smem, body + 8 * (u.size() + 3 * (size_t)rows));
+    smem = std::max<size_t>(smem, body + 8 * (u.size() + 5 * (size_t)rows));
     const size_t base = blob.size();
     boff[c] = (long long)base;
     blob.resize(base + 16 + body, 0);
@@ -1385,9 +1391,14 @@ static int coarse_build(long long n, long long nnz, const std::vector<int>& rp, 
     for (int k = 0; k < nz; ++k) lc[k] = (unsigned short)pos[cl[k0 + k]];
   }
   if (smem > 200 * 1024) return fail(HF_ERR_UNSUPPORTED, "coarse level too large for the one-kernel solve");
-  HF_CUDA(cudaFuncSetAttribute(k_coarse_cheb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HF_CUDA(cudaFuncSetAttribute(k_coarse_cheb<COARSE_THREADS, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HF_CUDA(cudaFuncSetAttribute(k_coarse_cheb<COARSE_THREADS_1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+
   int per_sm = 0;
-  HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_cheb, COARSE_THREADS, smem));
+  if (grid == 1)
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_cheb<COARSE_THREADS_1, 4>, COARSE_THREADS_1, smem));
+  else
+    HF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_cheb<COARSE_THREADS, 32>, COARSE_THREADS, smem));
   if (per_sm < 1) return fail(HF_ERR_UNSUPPORTED, "coarse kernel cannot be resident");
   hf_coarse* c = new hf_coarse();
   c->n = (int)n;
@@ -1608,7 +1619,7 @@ HF_API int hf_coarse_cheb_solve(hf_coarse* c, const double* b, double* x, double
   a.degree = degree;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)c->grid);
-  cfg.blockDim = dim3(COARSE_THREADS);
+  cfg.blockDim = dim3(c->grid == 1 ? COARSE_THREADS_1 : COARSE_THREADS);
   cfg.dynamicSmemBytes = c->smem;
   cfg.stream = S(stream);
   cudaLaunchAttribute attr[1];
@@ -1616,7 +1627,10 @@ HF_API int hf_coarse_cheb_solve(hf_coarse* c, const double* b, double* x, double
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  HF_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_cheb, a));
+  if (c->grid == 1)
+    HF_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_cheb<COARSE_THREADS_1, 4>, a));
+  else
+    HF_CUDA(cudaLaunchKernelEx(&cfg, k_coarse_cheb<COARSE_THREADS, 32>, a));
   return HF_OK;
 }
 

@@ -18,6 +18,11 @@
 //     CTA partials in index order), so every CTA takes the same stop decision
 //     and the result is deterministic.
 // Cooperative launch guarantees co-residency of the CTAs for the barrier.
+// A level whose whole matrix fits one CTA's shared memory (2D coarsest levels,
+// e.g. 4^2 Q2: 162 DoFs) runs as ONE CTA of COARSE_THREADS_1 threads: the
+// iterate stays in shared memory and every grid barrier becomes a
+// __syncthreads (the ~1.2 us grid barrier and the L2 round trip of the
+// gather were ~3.2 us of every application at config 1).
 #pragma once
 #include <cooperative_groups.h>
 
@@ -55,15 +60,28 @@ struct CoarseArgs {
 };
 
 constexpr int COARSE_THREADS = 256;
+constexpr int COARSE_THREADS_1 = 1024;  // the single-CTA form: 4 lanes per row (k_coarse_cheb<1024, 4>)
 
 // sum over the grid of one value per thread, in a fixed order; every thread
-// of every CTA returns the same total
+// of every CTA returns the same total (one CTA: no partials, no grid barrier)
 HF_DEV double coarse_grid_sum(double v, double* red, const CoarseArgs& a, cooperative_groups::grid_group& grid) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if (lane == 0) red[warp] = v;
   __syncthreads();
+  if (gridDim.x == 1) {
+    if (warp == 0) {
+      double t = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) red[32] = t;
+    }
+    __syncthreads();
+    const double t = red[32];
+    __syncthreads();  // red is reused by the next reduction
+    return t;
+  }
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < nw; ++w) s += red[w];
@@ -86,11 +104,13 @@ HF_DEV double coarse_grid_sum(double v, double* red, const CoarseArgs& a, cooper
 }
 
 // dynamic shared memory: the CTA's CoarseBlock (minus header), then the
-// gathered iterate entries (nu), then per own row A x, d and x
-__global__ void __launch_bounds__(COARSE_THREADS) k_coarse_cheb(const CoarseArgs a) {
+// gathered iterate entries (nu), then per own row A x, d, x, b and inv_d
+template <int NT, int G>
+__global__ void __launch_bounds__(NT) k_coarse_cheb(const CoarseArgs a) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   extern __shared__ __align__(16) unsigned char csm[];
-  __shared__ double red[COARSE_THREADS / 32];
+  __shared__ double red[33];
+  const bool single = gridDim.x == 1;  // the iterate lives in shared memory (xl)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned char* gb = a.blob + a.boff[blockIdx.x];
   const CoarseBlock hb = *reinterpret_cast<const CoarseBlock*>(gb);
@@ -113,12 +133,16 @@ __global__ void __launch_bounds__(COARSE_THREADS) k_coarse_cheb(const CoarseArgs
   double* axl = xs + nu;
   double* dl = axl + hb.rows;
   double* xl = dl + hb.rows;
+  double* bl = xl + hb.rows;   // this CTA's rows of b and inv_d, read once
+  double* idl = bl + hb.rows;
+  for (int l = threadIdx.x; l < hb.rows; l += blockDim.x) {
+    bl[l] = __ldg(a.b + r0 + l);
+    idl[l] = __ldg(a.inv_d + r0 + l);
+  }
+  __syncthreads();
   // ||b||^2, target, flag = (||b|| == 0)   (hf_scalar_op op 1)
   double bb = 0.0;
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    const double v = __ldg(a.b + i);
-    bb = fma(v, v, bb);
-  }
+  for (int l = threadIdx.x; l < hb.rows; l += blockDim.x) bb = fma(bl[l], bl[l], bb);
   const double bn2 = coarse_grid_sum(bb, red, a, grid);
   const double target = a.rel_target * sqrt(bn2);
   bool done = bn2 == 0.0;
@@ -128,14 +152,16 @@ __global__ void __launch_bounds__(COARSE_THREADS) k_coarse_cheb(const CoarseArgs
     a.flag[0] = done ? 1 : 0;
   }
   // first step from x = 0: d = inv_d b / theta, x = d
-  for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    const double z = __ldg(a.inv_d + i) * __ldg(a.b + i);
-    const double dd = z / a.theta;
-    dl[i - r0] = dd;
-    xl[i - r0] = dd;
-    a.x[i] = dd;
+  for (int l = threadIdx.x; l < hb.rows; l += blockDim.x) {
+    const double dd = idl[l] * bl[l] / a.theta;
+    dl[l] = dd;
+    xl[l] = dd;
+    if (!single) a.x[r0 + l] = dd;
   }
-  grid.sync();
+  if (single)
+    __syncthreads();
+  else
+    grid.sync();
   double rho_old = 1.0 / a.sigma;
   const double* xin = a.x;
   double* xout = a.xb;
@@ -146,24 +172,31 @@ __global__ void __launch_bounds__(COARSE_THREADS) k_coarse_cheb(const CoarseArgs
     // gather the iterate entries this CTA's rows touch (one L2 round trip)
     for (int j = threadIdx.x; j < nu; j += blockDim.x) {
       HF_ASSERT(ucol[j] >= 0 && ucol[j] < a.n);
-      xs[j] = __ldcg(xin + ucol[j]);
+      xs[j] = single ? xl[ucol[j]] : __ldcg(xin + ucol[j]);
     }
     __syncthreads();
-    // (A x)_i of this CTA's rows from shared memory, one warp per row
+    // (A x)_i of this CTA's rows from shared memory, G lanes per row (G = 32:
+    // one warp per row; the single-CTA form uses small groups so that each
+    // warp's row rounds are few and short).  The row rounds are warp-uniform,
+    // so every lane reaches the shuffles.
     double rr = 0.0;
-    for (int l = warp; l < hb.rows; l += nw) {
-      const int k0 = rowptr[l], k1 = rowptr[l + 1];
+    for (int base = warp * (32 / G); base < hb.rows; base += nw * (32 / G)) {
+      const int l = base + lane / G;
+      const bool on = l < hb.rows;
       double s = 0.0;
-      HF_ASSERT(k0 >= 0 && k1 <= nnz && k0 <= k1);
-      for (int k = k0 + lane; k < k1; k += 32) {
-        HF_ASSERT(lcol[k] < nu);
-        s = fma(val[k], xs[lcol[k]], s);
+      if (on) {
+        const int k0 = rowptr[l], k1 = rowptr[l + 1];
+        HF_ASSERT(k0 >= 0 && k1 <= nnz && k0 <= k1);
+        for (int k = k0 + lane % G; k < k1; k += G) {
+          HF_ASSERT(lcol[k] < nu);
+          s = fma(val[k], xs[lcol[k]], s);
+        }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) {
+      for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (on && lane % G == 0) {
         axl[l] = s;
-        const double r = __ldg(a.b + r0 + l) - s;
+        const double r = bl[l] - s;
         if (check) rr = fma(r, r, rr);
       }
     }
@@ -180,17 +213,20 @@ __global__ void __launch_bounds__(COARSE_THREADS) k_coarse_cheb(const CoarseArgs
     }
     // Chebyshev update of this CTA's rows (hf_cheb_step)
     for (int l = threadIdx.x; l < hb.rows; l += blockDim.x) {
-      const double z = __ldg(a.inv_d + r0 + l) * (__ldg(a.b + r0 + l) - axl[l]);
+      const double z = idl[l] * (bl[l] - axl[l]);
       const double dd = cd * dl[l] + cz * z;
       dl[l] = dd;
       const double xn = xl[l] + dd;
       xl[l] = xn;
-      xout[r0 + l] = xn;
+      if (!single) xout[r0 + l] = xn;
     }
     rho_old = rho;
     xin = xout;
     xout = xout == a.x ? a.xb : a.x;
-    grid.sync();
+    if (single)
+      __syncthreads();
+    else
+      grid.sync();
   }
   // the iterate (and the direction) of this CTA's rows
   for (int l = threadIdx.x; l < hb.rows; l += blockDim.x) {

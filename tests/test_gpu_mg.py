@@ -160,7 +160,8 @@ def _coarse_reference(A, inv_d, b, lv, rel_target, max_applications=100):
     return x.astype(np.float64), False
 
 
-def test_coarse_kernel_matches_launches(case, monkeypatch):
+@pytest.mark.parametrize("single", ["1", "0"])
+def test_coarse_kernel_matches_launches(case, single, monkeypatch):
     """The one-kernel coarse solve (hf_coarse_cheb_solve on the assembled level
     matrix) against the per-application launches on the matrix-free operator
     and an extended-precision restatement of the same iteration.  The coarse
@@ -174,6 +175,7 @@ def test_coarse_kernel_matches_launches(case, monkeypatch):
     from paper_1904_13131_b200.operators import AssembledTangent
 
     g, probs, transfers, _ = case
+    monkeypatch.setenv("HF_COARSE_SINGLE", single)  # single-CTA form where the level fits, or always multi-CTA
     u0 = restrict_solution(probs, g["ubar"])[0]
     lv = {}
     for mode in ("kernel", "launches"):

@@ -72,4 +72,7 @@ def test_gmg_cg_with_fp32_levels(name):
     x, rep = cg(op, g["b"], rel_tol=1e-8, preconditioner=gmg)
     assert rep.converged
     assert rep.iterations <= int(g["cg_iterations"]) + 2
-    assert rel(x, g["cg_solution"]) < 1e-6
+    # fp32 levels: BASELINE north_star's 1e-5 tolerance (the CG stops at
+    # ||r|| <= 1e-8 ||b||; the iterate's distance from the fp64 run's is
+    # cond(A) x that, ~1e-6 for these levels)
+    assert rel(x, g["cg_solution"]) < 1e-5
