@@ -39,7 +39,10 @@ def test_slab_decomposition_matches_single_gpu(nproc, m):
     for k in ("apply_scalar", "apply_tensor2", "apply_tensor4", "diagonal", "residual"):
         assert r[k] < 1e-12, (k, r[k])
     assert abs(r["cg_iterations_dist"] - r["cg_iterations_single"]) <= 1, r
-    assert r["cg_solution"] < 1e-6, r
+    # both solves stop at ||r|| <= 1e-8 ||b||; their iterates differ by up to
+    # cond(A) times that (measured 0.3e-6 .. 1.6e-6 run to run: the atomic
+    # scatter order differs between runs and the CG amplifies it)
+    assert r["cg_solution"] < 1e-5, r
 
 
 @pytest.mark.gpu
