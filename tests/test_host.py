@@ -89,3 +89,25 @@ def test_sub_box_partition_roundtrip():
     assert np.array_equal(np.concatenate([pp.material_id for pp in parts]), msh.material_id)
     assert parts[1].cell_offset == (0, 0, 3)
     assert np.allclose(parts[1].vertices[0], [0, 0, 3 / 8])
+
+
+@pytest.mark.parametrize("dim,m,p", [(2, 5, 2), (3, 4, 2), (3, 3, 4), (2, 4, 3), (3, 2, 1)])
+def test_node_coordinates_separable_matches_cell_map(dim, m, p):
+    """node_coordinates refines the vertex lattice axis by axis; it equals the
+    per-cell multilinear map (fespace.py:142-151) evaluated at every cell's
+    local nodes, also on a perturbed mesh."""
+    import dataclasses
+
+    msh = mesh.build_benchmark_mesh(dim, m, [], side=1.0)
+    rng = np.random.default_rng(3)
+    msh = dataclasses.replace(msh, vertices=msh.vertices + 0.02 * rng.standard_normal(msh.vertices.shape))
+    dm = fespace.build_dof_map(msh, p, dim)
+    loc = fespace.lex_grid_points([np.arange(p + 1) / p] * dim)
+    off = fespace.lex_grid_indices((2,) * dim)
+    q1 = np.ones((2**dim, len(loc)))
+    for k in range(dim):
+        q1 *= np.where(off[:, k:k + 1] == 1, loc[None, :, k], 1.0 - loc[None, :, k])
+    per_el = np.einsum("eci,cn->eni", msh.element_corners(), q1)
+    ref = np.zeros((dm.n_nodes, dim))
+    ref[dm.cell_nodes.reshape(-1)] = per_el.reshape(-1, dim)
+    assert np.allclose(fespace.node_coordinates(msh, dm), ref, rtol=0, atol=1e-15)
