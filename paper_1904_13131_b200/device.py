@@ -83,15 +83,25 @@ def capture_graph(fn) -> torch.cuda.CUDAGraph:
     emptying the cache each time sent every later allocation back to
     cudaMalloc.  Capturing with ``capture_begin/capture_end`` directly keeps
     the cache."""
+    import gc
+
     g = torch.cuda.CUDAGraph()
     cur = torch.cuda.current_stream()
     side = torch.cuda.Stream()
     side.wait_stream(cur)
-    with torch.cuda.stream(side):
-        g.capture_begin()
-        try:
-            fn()
-        finally:
-            g.capture_end()
+    # no cyclic GC while capturing: a collected libhf handle would free device
+    # memory (a device synchronisation) in the middle of the capture
+    was_enabled = gc.isenabled()
+    gc.disable()
+    try:
+        with torch.cuda.stream(side):
+            g.capture_begin()
+            try:
+                fn()
+            finally:
+                g.capture_end()
+    finally:
+        if was_enabled:
+            gc.enable()
     cur.wait_stream(side)
     return g
