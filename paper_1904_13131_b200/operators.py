@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import device as dv
-from ._lib import HF_ERR_JACOBIAN, STRATEGY_CODE, HfErrorInfo, check, lib
+from ._lib import HF_ERR_ARG, HF_ERR_JACOBIAN, STRATEGY_CODE, HfErrorInfo, check, lib
 from .fespace import (ConstraintSet, bottom_constraints, build_dof_map, gauss_legendre, lagrange_basis)
 from .material import NeoHookeanParams, NonPositiveJacobian, n_sym
 from .mesh import INCLUSION, Mesh, MeshHierarchy, lex_grid_indices, lex_grid_points
@@ -355,9 +355,12 @@ class MatrixFreeTangent:
         numpy in -> numpy out; CUDA tensor in -> CUDA tensor out; a pinned CPU
         tensor in with a pinned ``out`` runs the host-to-host pipeline
         (``apply_host``)."""
-        if (out is not None and isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned()
-                and out.is_pinned() and self.storage == "fp64"):
-            return self.apply_host(x, out)
+        if (out is not None and isinstance(x, torch.Tensor) and isinstance(out, torch.Tensor) and not x.is_cuda
+                and not out.is_cuda and self.storage == "fp64"):
+            # host tensors: the host pipeline when both are page-locked (libhf
+            # checks that itself, so no torch is_pinned() queries on this path)
+            if self._apply_host(x, out, 4, must=False):
+                return out
         xd = dv.as_dev(x)
         if self.storage == "fp32":  # the public apply stays fp64 in, fp64 out
             y32 = torch.empty(xd.shape, dtype=torch.float32, device="cuda")
@@ -377,13 +380,24 @@ class MatrixFreeTangent:
         H2D copy of each slab's node planes, the slab's cell kernel and the D2H
         copy of finished planes overlap on three streams; the pipeline is a
         CUDA graph captured on first use per buffer pair and replayed after."""
+        self._apply_host(xh, yh, chunks, must=True)
+        return yh
+
+    def _apply_host(self, xh: torch.Tensor, yh: torch.Tensor, chunks: int, must: bool) -> bool:
+        """hf_tangent_apply_host + stream synchronisation.  With ``must=False``
+        returns False (nothing run) when the buffers are not page-locked."""
         if xh.dtype != torch.float64 or yh.dtype != torch.float64 or xh.numel() != self.n_dofs \
                 or yh.numel() != self.n_dofs or not (xh.is_contiguous() and yh.is_contiguous()):
-            raise ValueError("apply_host needs contiguous float64 host vectors of n_dofs entries")
-        check(lib().hf_tangent_apply_host(self._op, ct.c_void_p(xh.data_ptr()), ct.c_void_p(yh.data_ptr()), chunks,
-                                          dv.stream()))
-        torch.cuda.current_stream().synchronize()
-        return yh
+            if must:
+                raise ValueError("apply_host needs contiguous float64 host vectors of n_dofs entries")
+            return False
+        s = torch.cuda.current_stream()
+        rc = lib().hf_tangent_apply_host(self._op, xh.data_ptr(), yh.data_ptr(), chunks, s.cuda_stream)
+        if rc == HF_ERR_ARG and not must:
+            return False  # not page-locked: the caller copies through device buffers
+        check(rc)
+        s.synchronize()
+        return True
 
     def host_info(self) -> dict:
         """How the host pipeline runs on this host (hf_tangent_host_info): the

@@ -94,6 +94,13 @@ def test_pinned_host_apply_pipeline_matches_device_apply():
         op.apply(xh, out=yh)
         assert _rel(yh.cuda(), yd) < 1e-14
         assert torch.equal(yh[wl.fine.constraints.mask], xh[wl.fine.constraints.mask])
+    # pageable host tensors (or one of them): the device-buffer path, same result
+    xp, yp = xh.clone(), torch.empty_like(xh)
+    assert not xp.is_pinned() and not yp.is_pinned()
+    for x_, y_ in ((xp, yp), (xh, yp), (xp, yh)):
+        y_.zero_()
+        assert op.apply(x_, out=y_) is y_
+        assert _rel(y_.cuda(), yd) < 1e-14
 
 
 @pytest.mark.parametrize("cfg,m", [(1, None), (2, 6), (3, 3)])
