@@ -309,22 +309,26 @@ template <typename TI = double, typename TO = double>
 __global__ void k_axis(const TI* __restrict__ in, TO* __restrict__ out, int n0, int n1, int n2, int C, int axis,
                        int nout, const int* __restrict__ rowptr, const int* __restrict__ cols,
                        const double* __restrict__ w, const uint8_t* __restrict__ mask, int mode) {
-  int m0 = axis == 0 ? nout : n0, m1 = axis == 1 ? nout : n1, m2 = axis == 2 ? nout : n2;
-  long long total = (long long)m0 * m1 * m2 * C;
-  long long in_stride = axis == 0 ? C : (axis == 1 ? (long long)n0 * C : (long long)n0 * n1 * C);
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    long long r = t;
-    int c = (int)(r % C);
-    r /= C;
-    int i0 = (int)(r % m0);
+  // 32-bit index arithmetic: both lattices hold < 2^31 DoFs (hf_space_create),
+  // and 32-bit divisions by the run-time extents are a fraction of the cost of
+  // 64-bit ones (four per element)
+  const unsigned m0 = axis == 0 ? nout : n0, m1 = axis == 1 ? nout : n1, m2 = axis == 2 ? nout : n2;
+  const unsigned total = m0 * m1 * m2 * (unsigned)C;
+  const unsigned in_stride = axis == 0 ? C : (axis == 1 ? (unsigned)n0 * C : (unsigned)n0 * n1 * C);
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    unsigned r = t;
+    const unsigned c = r % (unsigned)C;
+    r /= (unsigned)C;
+    const unsigned i0 = r % m0;
     r /= m0;
-    int i1 = (int)(r % m1);
-    int i2 = (int)(r / m1);
-    int o = axis == 0 ? i0 : (axis == 1 ? i1 : i2);
-    long long base = (((long long)(axis == 2 ? 0 : i2) * n1 + (axis == 1 ? 0 : i1)) * n0 + (axis == 0 ? 0 : i0)) * C + c;
+    const unsigned i1 = r % m1;
+    const unsigned i2 = r / m1;
+    const unsigned o = axis == 0 ? i0 : (axis == 1 ? i1 : i2);
+    const unsigned base = (((axis == 2 ? 0u : i2) * (unsigned)n1 + (axis == 1 ? 0u : i1)) * (unsigned)n0 +
+                           (axis == 0 ? 0u : i0)) * (unsigned)C + c;
     double s = 0.0;
     for (int k = rowptr[o]; k < rowptr[o + 1]; ++k)
-      s = fma(w[k], (double)in[base + (long long)cols[k] * in_stride], s);
+      s = fma(w[k], (double)in[base + (unsigned)cols[k] * in_stride], s);
     if (mode == 0) out[t] = (TO)s;
     else if (mode == 1) out[t] = mask[t] ? (TO)0 : (TO)s;
     else if (!mask[t]) out[t] = (TO)((double)out[t] + s);
