@@ -155,6 +155,9 @@ def _time_steps(local_op, x, y, steps, warmup, flush, step_fn=None, flush_l2=Tru
     return float(np.mean(step)), launches
 
 
+E2E_WARMUP_STEPS = 1000
+
+
 def _e2e(apply_into, x_host: np.ndarray, steps, warmup, public_apply=None):
     """Through the public apply: pinned H2D of x, tangent apply, D2H of y, every
     step.  ``public_apply(xh, out=yh)`` is MatrixFreeTangent.apply on pinned
@@ -174,7 +177,12 @@ def _e2e(apply_into, x_host: np.ndarray, steps, warmup, public_apply=None):
         apply_into(xd, yd)
         yh.copy_(yd, non_blocking=True)
 
-    for _ in range(warmup):
+    # warm-up: max(warmup, E2E_WARMUP_STEPS) steps (~0.3-0.6 s; a fixed count,
+    # so every rank runs the same number of interface exchanges).  Host-link
+    # step times on these boxes run ~1.7x slow for tens of milliseconds at a
+    # time before settling (tools/e2e_plain_vs_piped.py, DESIGN.md e2e); the
+    # timed steps are the settled, steady-state ones a serving loop sees.
+    for _ in range(max(warmup, E2E_WARMUP_STEPS)):
         one()
     torch.cuda.synchronize()
     t = []
@@ -340,7 +348,7 @@ def run_ours(args):
         step_ms, kern_ms = t.tolist()
     ab = algorithmic_bytes("tensor4", 3, prob.n_dofs, nqp)
     apply_into = public.apply_into if public is not None else op.apply_into
-    e2e_steps = max(args.steps, 10)
+    e2e_steps = max(args.steps, 200)  # the host link drifts between slow and fast windows: a longer median
     e2e_ms, h2d, d2h = _e2e(apply_into, x_host, e2e_steps, args.warmup,
                             public_apply=op.apply if public is None else None)
     if ws > 1:
@@ -367,7 +375,9 @@ def run_ours(args):
                                                    f"{algorithmic_bytes('tensor4', 3, prob.n_dofs, nqp, True)} B)",
                          "kernel_ms": kern_ms, "kernel": KERNEL},
             "e2e": {"value": n_global / e2e_ms / 1e6, "unit": "GDoF/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "stat": f"median of {e2e_steps} synchronised steps",
+                    "d2h_bytes_per_step": d2h,
+                    "stat": f"median of {e2e_steps} synchronised steps after "
+                            f"{max(args.warmup, E2E_WARMUP_STEPS)} warm-up steps",
                     "pipeline": op.host_info() if public is None and hasattr(op, "host_info") else None},
             "gpu_launches": launches * args.steps, "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_extra:
@@ -438,7 +448,7 @@ def _cfg1(cpu: bool):
     amplitude 0.005.  One tensor4 vmult on the seeded N(0,1) vector,
     and one GMG-preconditioned CG solve of b = A x (constrained entries 0) to
     rtol 1e-8 with the degree-4 Chebyshev smoother; GMG build + solve run
-    twice, the warm run reported.  With ``cpu``, the oracle port of the same
+    four times, the median of the three warm runs reported.  With ``cpu``, the oracle port of the same
     setup and solve on one host core beside it (the reference pkg "runs this
     directly"; SURVEY P5 measured 0.9 s setup + 6.8 s solve)."""
     import torch
@@ -466,8 +476,8 @@ def _cfg1(cpu: bool):
     b = op.apply(x)
     b[fine.mask_dev] = 0.0
     transfers = build_transfers(probs)
-    rec = None
-    for _ in range(2):
+    recs = []
+    for run in range(4):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         gmg = build_gmg(probs, u, "tensor4", seed=0, transfers=transfers)
@@ -481,7 +491,13 @@ def _cfg1(cpu: bool):
                "vmult_note": f"mean of {reps} back-to-back applies (the 2.9 MB working set is L2-resident)",
                "gmg_setup_s": t1 - t0, "cg_solve_s": t2 - t1, "cg_iterations": rep.iterations,
                "s_per_cg_iteration": (t2 - t1) / max(rep.iterations, 1)}
+        if run > 0:  # the first run is the cold one
+            recs.append(rec)
         del gmg
+    # a ~15 ms host-driven solve is sensitive to the box's host: the warm run
+    # with the median solve time of three
+    rec = sorted(recs, key=lambda r: r["cg_solve_s"])[len(recs) // 2]
+    rec["stat"] = "median (by cg_solve_s) of 3 warm GMG build + solve runs"
     if cpu:
         from threadpoolctl import threadpool_limits
 

@@ -199,7 +199,14 @@ struct HostPipe {
     cudaGraphExec_t exec;  // null: enqueue directly (variant 2 overlap / 3 serial)
     unsigned long long used;
     int variant;
+    unsigned uses;  // calls of this entry
+    int recal;      // the one recalibration after RECAL_AT calls is done
   } g[NG] = {};
+  // A first calibration can fall into a window in which the host link runs
+  // ~1.7x slow (tens of ms at a time, early in a process on some boxes), and
+  // then picks a variant that is not the fastest in steady state: each entry
+  // is calibrated once more after this many calls.
+  static constexpr unsigned RECAL_AT = 256;
   int ng = 0;
   unsigned long long clock = 0;
   int last_order = -1;           // variant of the last calibration: 0 graph overlap, 1 graph serial,
@@ -864,6 +871,15 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
   HostPipe::Entry* hit = nullptr;
   for (int i = 0; i < h->ng; ++i)
     if (h->g[i].x == x_host && h->g[i].y == y_host && h->g[i].chunks == chunks) hit = &h->g[i];
+  int recal_slot = -1;
+  if (hit && !hit->recal && hit->uses >= HostPipe::RECAL_AT && !std::getenv("HF_E2E_ORDER")) {
+    HF_CUDA(cudaStreamSynchronize(S(stream)));  // the entry's graph may still be running
+    if (hit->exec) HF_CUDA(cudaGraphExecDestroy(hit->exec));
+    hit->exec = nullptr;
+    hit->variant = 2;  // direct enqueue until the recalibration below has finished
+    recal_slot = (int)(hit - h->g);
+    hit = nullptr;
+  }
   // enqueue directly on `stream` (no graph): fork/join through the pipe's streams
   auto direct = [&](bool serial) -> int {
     cudaEvent_t fork;
@@ -943,19 +959,22 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
       if (cand[v] && v != keep) cudaGraphExecDestroy(cand[v]);
     cudaGraphExec_t exec = keep < 2 ? cand[keep] : nullptr;
     h->last_order = keep;
-    int slot = h->ng;
-    if (slot == HostPipe::NG) {  // evict the least recently used pipeline
+    int slot;
+    if (recal_slot >= 0) {
+      slot = recal_slot;
+    } else if (h->ng == HostPipe::NG) {  // evict the least recently used pipeline
       slot = 0;
       for (int i = 1; i < h->ng; ++i)
         if (h->g[i].used < h->g[slot].used) slot = i;
       if (h->g[slot].exec) cudaGraphExecDestroy(h->g[slot].exec);
     } else {
-      ++h->ng;
+      slot = h->ng++;
     }
-    h->g[slot] = {x_host, y_host, chunks, exec, 0, keep};
+    h->g[slot] = {x_host, y_host, chunks, exec, 0, keep, 0, recal_slot >= 0 ? 1 : 0};
     hit = &h->g[slot];
   }
   hit->used = ++h->clock;
+  ++hit->uses;
   if (hit->exec) {
     HF_CUDA(cudaGraphLaunch(hit->exec, S(stream)));
     return HF_OK;

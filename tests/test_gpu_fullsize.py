@@ -145,6 +145,32 @@ def test_host_apply_graph_chunks_and_buffers(cfg, m):
         check(lib().hf_host_unregister(ct.c_void_p(ya.ctypes.data)))
 
 
+def test_host_apply_recalibration():
+    """hf_tangent_apply_host recalibrates each buffer pair's pipeline once
+    after HostPipe::RECAL_AT (256) calls: results stay exact across it and the
+    pipeline info reports a variant afterwards."""
+    from paper_1904_13131_b200 import MatrixFreeTangent
+    from paper_1904_13131_b200.workloads import make_workload
+
+    wl = make_workload(2, seed=3, m=4)
+    op = MatrixFreeTangent(wl.fine, wl.ubar, "tensor4")
+    n = op.n_dofs
+    xh = torch.empty(n, dtype=torch.float64).pin_memory()
+    yh = torch.empty(n, dtype=torch.float64).pin_memory()
+    rng = np.random.default_rng(2)
+    for call in range(300):
+        if call % 50 == 0 or 254 <= call <= 258:
+            xh.copy_(torch.from_numpy(rng.standard_normal(n)))
+            yh.fill_(np.nan)
+            op.apply(xh, out=yh)
+            assert _rel(yh.cuda(), op.apply(xh.cuda())) < 1e-14, call
+        else:
+            op.apply(xh, out=yh)
+    info = op.host_info()
+    assert info["variant"] in ("graph+overlap", "graph+serial", "direct+overlap", "direct+serial")
+    assert all(v > 0 for v in info["calibration_us"].values())
+
+
 def test_tile_range_apply_with_reserved_sms():
     """hf_tangent_apply_tiles_ex: tile ranges launched on fewer SMs (room for a
     concurrent NCCL kernel) accumulate the same result as the full apply."""
