@@ -159,7 +159,10 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
  * back until the last H2D is done.  On first use per buffer pair all four are
  * timed on this host and the fastest kept (hosts differ: on some, concurrent
  * H2D + D2H is slower than back to back, or a graph with host-memory copy
- * nodes launches slower than direct enqueues).  HF_E2E_ORDER=0..3 forces one.
+ * nodes launches slower than direct enqueues).  Each buffer pair is timed
+ * once more on its 257th call (a first calibration can land in a slow window
+ * of the host link).  The calls that calibrate synchronise `stream`.
+ * HF_E2E_ORDER=0..3 forces one variant and turns calibration off.
  * hf_tangent_host_info: the variant kept by the last calibration (0 graph +
  * overlap, 1 graph + serial, 2 direct + overlap, 3 direct + serial, -1 none)
  * and the four measured step times in us (us4[4], 0 if not measured). */
