@@ -5,26 +5,29 @@ operator on B200, plus the GMG-CG Newton-step time.
 
 One step = one tangent application (tensor4 cache, the paper's "Algorithm 3")
 through ``MatrixFreeTangent.apply`` semantics: y = mask ? x : 0, the cell
-kernel, and for N > 1 the interface exchange.  Workload: BASELINE config 2
-(3D 32^3 Q2, 823,875 DoFs per GPU, seeded synthetic inputs).
+kernel, and for N > 1 the interface exchange.
 
-* N = 1: the config-2 mesh itself.
-* N > 1 (torchrun, one rank per GPU, NCCL): weak scaling over slabs.  The
-  global mesh is N config-2 cubes stacked along z (32 x 32 x 32N cells); each
-  rank owns one 32-layer slab.  The interface reverse-add (NCCL send/recv +
-  hf_halo_add) is inside the timed step.  ``value`` = global DoFs / the max
-  over ranks of the step time.
+* N = 1: BASELINE config 2 (3D 32^3 Q2, 823,875 DoFs; seeded synthetic
+  inputs), ``scaling: weak``.
+* N > 1 (one rank per GPU over NCCL; ``--gpus N`` without torchrun starts the
+  N ranks itself through torch.distributed.run): BASELINE config 5 (128^3 Q2,
+  50,923,779 DoFs) as strong scaling over z-slabs, ``value`` = global DoFs /
+  the max over ranks of the step time; the interface reverse-add (NCCL
+  send/recv + hf_halo_add) is inside the step.  The config-5 record adds the
+  10-iteration GMG-CG with exchange and all-reduce times; ``cfg2_weak`` is N
+  config-2 cubes stacked along z, one per GPU.
 
-The headline steps run back to back: the 262 MB tensor4 cache exceeds the
-126 MB L2, so every step streams it from HBM (``config.l2``); the same step
-with a 256 MiB L2 flush before each is reported beside it.  The extras
-(tensor2/scalar caches of 45-127 MB, which L2 could hold) flush before every
-step.  CUDA events on the launching stream.  ``roofline`` uses the kernel-only event
-pair around the cell kernel.  At N = 1 rank 0 adds: the other caching
-variants, config 3 (16^3 Q4), one config-4 Newton iteration (64^3, GMG levels
-4..64), the measured fp64 peak, and the CPU baseline (the oracle port).
-``--impl reference`` times the reference algorithm's CPU port (oracle/) on all
-host cores: the reference is pure Python and absent on the GPU box.
+The headline steps run back to back: the tensor4 cache exceeds the 126 MB L2,
+so every step streams it from HBM (``config.l2``); the same step with a
+256 MiB L2 flush before each is reported beside it (``l2_flushed``).  The
+extras (tensor2/scalar caches of 45-127 MB, which L2 could hold) flush before
+every step.  CUDA events on the launching stream.  ``roofline`` uses the
+kernel-only event pair around the cell kernel.  At N = 1 rank 0 adds: the
+other caching variants, config 3 (16^3 Q4), config 1, config 4 Newton, config
+5 on one GPU, the measured fp64 peak, and the CPU baseline: the unmodified
+reference's own apply (``oracle/_ref``, installed by ``oracle/build_ref.py``)
+on one host core.  ``--impl reference`` times that reference apply on all host
+cores, with the same ``config``.
 """
 
 from __future__ import annotations
@@ -161,7 +164,8 @@ E2E_WARMUP_STEPS = 1000
 def _e2e(apply_into, x_host: np.ndarray, steps, warmup, public_apply=None):
     """Through the public apply: pinned H2D of x, tangent apply, D2H of y, every
     step.  ``public_apply(xh, out=yh)`` is MatrixFreeTangent.apply on pinned
-    host tensors (slab-pipelined copies and kernel); otherwise copy, apply_into, copy."""
+    host tensors (slab-pipelined copies and kernel); otherwise copy, apply_into, copy.
+    Returns ({median, mean, p90, ...} ms, h2d bytes, d2h bytes)."""
     import torch
 
     xh = torch.from_numpy(x_host.copy()).pin_memory()
@@ -180,21 +184,48 @@ def _e2e(apply_into, x_host: np.ndarray, steps, warmup, public_apply=None):
     # warm-up: max(warmup, E2E_WARMUP_STEPS) steps (~0.3-0.6 s; a fixed count,
     # so every rank runs the same number of interface exchanges).  Host-link
     # step times on these boxes run ~1.7x slow for tens of milliseconds at a
-    # time before settling (tools/e2e_plain_vs_piped.py, DESIGN.md e2e); the
-    # timed steps are the settled, steady-state ones a serving loop sees.
+    # time (tools/e2e_plain_vs_piped.py, DESIGN.md e2e): the median is the
+    # steady state, the mean and p90 show the slow windows.
     for _ in range(max(warmup, E2E_WARMUP_STEPS)):
         one()
     torch.cuda.synchronize()
+    t = _event_steps(one, steps)
+    return _stats(t), xh.numel() * 8, yh.numel() * 8
+
+
+def _event_steps(fn, steps):
+    """Per-step device time (ms) of ``fn`` between CUDA events, synchronised each step."""
+    import torch
+
     t = []
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        one()
+        fn()
         e1.record()
         torch.cuda.synchronize()
         t.append(e0.elapsed_time(e1))
-    # median: single steps over the host link are noisy (e2e)
-    return float(np.median(t)), xh.numel() * 8, yh.numel() * 8
+    return t
+
+
+def _stats(t):
+    return {"median": float(np.median(t)), "mean": float(np.mean(t)), "p90": float(np.percentile(t, 90)),
+            "min": float(np.min(t)), "max": float(np.max(t)), "n": len(t)}
+
+
+def _e2e_ndarray(op, x_host: np.ndarray, steps: int):
+    """The reference calling convention itself: ``y = op.apply(x)`` with a
+    pageable numpy x and a fresh numpy y (operators.py:331-339), timed on the
+    host clock around each synchronous call."""
+    for _ in range(10):
+        op.apply(x_host)
+    t = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        y = op.apply(x_host)
+        t.append((time.perf_counter() - t0) * 1e3)
+    assert isinstance(y, np.ndarray)
+    return _stats(t)
 
 
 def fp64_peak():
@@ -218,8 +249,30 @@ def fp64_peak():
     return 16.0 * iters * blocks * threads / (e0.elapsed_time(e1) * 1e-3) / 1e12
 
 
-def _oracle_apply(cfg_id=2, strategy="tensor4"):
-    """The reference algorithm's CPU port (oracle/) set up on a config: returns (apply, x, DoFs)."""
+def _config(ws: int) -> dict:
+    """The workload of the headline line; the reference arm prints the same dict."""
+    if ws == 1:
+        return {"workload": "cfg2 3D 32^3 Q2 tensor4 tangent vmult (823,875 DoFs)", "strategy": "tensor4",
+                "l2": "inputs larger than L2: the 262 MB q-point cache exceeds the 126 MB L2 and is streamed "
+                      "from HBM every step (x, y: 13 MB); steps timed back to back",
+                "parallelism": "single GPU"}
+    return {"workload": f"cfg5 3D 128^3 Q2 tensor4 tangent vmult (50,923,779 DoFs), strong scaling over {ws} GPUs",
+            "strategy": "tensor4",
+            "l2": "inputs larger than L2: the 16.8 GB q-point cache (2.1-8.4 GB per GPU) is streamed from HBM "
+                  "every step; steps timed back to back",
+            "parallelism": f"z-slab cell partition x{ws}, NCCL interface reverse-add + dot all-reduce"}
+
+
+def _ref_apply(cfg_id=2, strategy="tensor4"):
+    """The UNMODIFIED reference (oracle/_ref) set up on a config: (apply, x, DoFs, kind, what).
+    Falls back to the oracle port when the installed reference is absent."""
+    from oracle import ref
+
+    if ref.available():
+        hf, prob, ubar, x = ref.config_problem(cfg_id, seed=0, amp=0.05)
+        op = hf.operators.MatrixFreeTangent(prob, ubar, strategy)
+        return op.apply, x, prob.n_dofs, "reference", (
+            f"hyperfree 0.1.0 (the unmodified reference, oracle/_ref) MatrixFreeTangent.apply, cfg{cfg_id} {strategy}")
     from oracle import hf_oracle as O
     from paper_1904_13131_b200.workloads import AMP_VMULT, MATERIAL, host_workload
 
@@ -231,17 +284,17 @@ def _oracle_apply(cfg_id=2, strategy="tensor4"):
     prob = O.OProblem(mesh.dim, hw.cfg["degree"], mesh.cells, mesh.vertices, mu, lam, hw.masks[-1])
     prob.geometry()
     op = O.Tangent(prob, hw.ubar, strategy)
-    return op.apply, hw.x, prob.n_dofs
+    return op.apply, hw.x, prob.n_dofs, "port", f"oracle/hf_oracle.py numpy port of the reference apply, cfg{cfg_id}"
 
 
 def cpu_baseline(cfg_id=2, strategy="tensor4", budget_s=20.0, threads=1):
-    """Oracle port on a bounded sample: setup, 1 warm-up apply (bench.py:206
-    convention), then applies until the budget (>= 1, <= 10).  Returns
-    (GDoF/s, s per apply, applies, DoFs)."""
+    """The reference's own apply on a bounded sample: setup, 1 warm-up apply
+    (the reference bench.py:206 convention), then applies until the budget
+    (>= 1, <= 10).  Returns (GDoF/s, s per apply, applies, DoFs, kind, what)."""
     from threadpoolctl import threadpool_limits
 
     with threadpool_limits(threads):
-        apply, x, ndofs = _oracle_apply(cfg_id, strategy)
+        apply, x, ndofs, kind, what = _ref_apply(cfg_id, strategy)
         apply(x)
         t0 = time.perf_counter()
         n = 0
@@ -249,21 +302,28 @@ def cpu_baseline(cfg_id=2, strategy="tensor4", budget_s=20.0, threads=1):
             apply(x)
             n += 1
         dt = (time.perf_counter() - t0) / n
-    return ndofs / dt / 1e9, dt, n, ndofs
+    return ndofs / dt / 1e9, dt, n, ndofs, kind, what
 
 
 def run_reference(args):
-    """The reference algorithm's CPU implementation (the oracle port; the reference
-    is pure Python and absent on the GPU box) on all host cores; one step = one
-    apply of config 2, W warm-up steps, then up to K timed steps (bounded to ~90 s)."""
+    """The reference's own CPU implementation of the path (the unmodified
+    hyperfree package installed in oracle/_ref; the oracle port only if that is
+    missing) on all host cores.  One step = one MatrixFreeTangent.apply of the
+    config-2 problem (at N > 1, where the whole config-5 problem does not fit a
+    host -- SURVEY H9 -- the config-2-sized block of it is the bounded sample);
+    W warm-up steps (at most 1), then up to K timed steps, bounded to ~90 s."""
     from threadpoolctl import threadpool_limits
+
+    from oracle import ref
 
     ws, rank, _ = _dist()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     with threadpool_limits(threads):
-        apply, x, ndofs = _oracle_apply(2, "tensor4")
+        t_setup = time.perf_counter()
+        apply, x, ndofs, kind, what = _ref_apply(2, "tensor4")
+        t_setup = time.perf_counter() - t_setup
         for _ in range(min(args.warmup, 1)):
             apply(x)
         times = []
@@ -273,134 +333,171 @@ def run_reference(args):
             times.append(time.perf_counter() - t0)
     dt = float(np.mean(times))
     v = ndofs / dt / 1e9
+    sample = (f"{what}: {len(times)} timed applies of the 823,875-DoF cfg2 problem after {min(args.warmup, 1)} "
+              f"warm-up (setup {t_setup:.1f} s untimed), numpy/OpenBLAS with {threads} threads allowed")
+    if args.gpus > 1:
+        sample += "; a cfg2-sized block stands in for the cfg5 problem, which exceeds host memory (SURVEY H9)"
     line = {"metric": METRIC, "value": v, "unit": "GDoF/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": len(times), "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg2 3D 32^3 Q2 tensor4 tangent vmult (823,875 DoFs)", "strategy": "tensor4"},
-            "cpu_baseline": {"value": v, "unit": "GDoF/s", "cores": threads, "kind": "port",
-                             "sample": "oracle/hf_oracle.py (numpy restatement of the reference operators.py:331-393, "
-                                       f"pinned to reference golden vectors): {len(times)} timed applies of cfg2 after "
-                                       "1 warm-up"},
+            "scaling": "weak" if args.gpus == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(args.gpus),
+            "cpu_baseline": {"value": v, "unit": "GDoF/s", "cores": threads, "kind": kind, "sample": sample,
+                             "cpu_model": ref.cpu_model(), "host_cpus": os.cpu_count()},
             "e2e": {"value": v, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _init_dist(ws, local):
+    import torch
+
+    if ws == 1:
+        torch.cuda.set_device(0)
+        return
+    import torch.distributed as dist
+
+    # HF_BENCH_BACKEND=gloo runs the N>1 code path with every rank on one
+    # GPU (exchange staged through the host) -- a functional check only
+    backend = os.environ.get("HF_BENCH_BACKEND", "nccl")
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group(backend)
+
+
+def _headline_single(args, flush):
+    """N = 1: config 2 on one GPU through MatrixFreeTangent."""
+    import torch
+
+    from paper_1904_13131_b200 import MatrixFreeTangent
+    from paper_1904_13131_b200.workloads import make_workload
+
+    wl = make_workload(2, seed=0)
+    prob = wl.fine
+    op = MatrixFreeTangent(prob, wl.ubar, "tensor4")
+    x = torch.from_numpy(wl.x).cuda()
+    y = torch.empty_like(x)
+    torch.cuda.synchronize()
+    with Clocks(torch.cuda.current_device()) as clk:
+        kern_ms, launches = _time_steps(op, x, y, args.steps, args.warmup, flush, flush_l2=False)
+    flushed_ms, _ = _time_steps(op, x, y, max(args.steps // 2, 5), 3, flush)
+    e2e, h2d, d2h = _e2e(op.apply_into, wl.x, max(args.steps, 200), args.warmup, public_apply=op.apply)
+    e2e_nd = _e2e_ndarray(op, wl.x, 50)
+    return dict(prob=prob, ubar=wl.ubar, x=x, y=y, n_global=prob.n_dofs, step_ms=kern_ms, kern_ms=kern_ms,
+                flushed_ms=flushed_ms, launches=launches, clk=clk, e2e=e2e, h2d=h2d, d2h=d2h, e2e_ndarray=e2e_nd,
+                pipeline=op.host_info())
 
 
 def run_ours(args):
     import torch
 
     ws, rank, local = _dist()
-    if ws > 1:
-        import torch.distributed as dist
-
-        # HF_BENCH_BACKEND=gloo runs the N>1 code path with every rank on one
-        # GPU (exchange staged through the host) -- a functional check only
-        backend = os.environ.get("HF_BENCH_BACKEND", "nccl")
-        dev = local % torch.cuda.device_count()
-        torch.cuda.set_device(dev)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        else:
-            dist.init_process_group(backend)
-    else:
-        torch.cuda.set_device(0)
-    from paper_1904_13131_b200 import MatrixFreeTangent
-    from paper_1904_13131_b200.distributed import DistProblem, DistributedTangent, Slab, TorchComm, slab_ranges
-    from paper_1904_13131_b200.workloads import MATERIAL, algorithmic_bytes, host_workload, make_workload, meter_flops
+    _init_dist(ws, local)
+    from paper_1904_13131_b200.distributed import LocalComm, TorchComm
+    from paper_1904_13131_b200.workloads import algorithmic_bytes
 
     hbm, peak_kind = _peaks()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    exchange = None
+    cfg5 = None
     if ws == 1:
-        wl = make_workload(2, seed=0)
-        prob, ubar, x_host = wl.fine, wl.ubar, wl.x
-        n_global = prob.n_dofs
-        make_op = lambda s: MatrixFreeTangent(prob, ubar, s)  # noqa: E731
-        public = None
+        h = _headline_single(args, flush)
     else:
         comm = TorchComm()
-        hw = host_workload(2, seed=0, stack=ws)
-        cells = hw.meshes[-1].cells
-        slab = Slab(3, 2, cells, *slab_ranges(cells[-1], ws)[rank])
-        dp = DistProblem(hw.meshes[-1], 2, MATERIAL, slab, comm, hw.masks[-1])
-        prob, ubar, x_host = dp.local, np.ascontiguousarray(slab.local(hw.ubar)), np.ascontiguousarray(slab.local(hw.x))
-        n_global = slab.n_global_dofs
-        exchange = dp.exchange
-        public = DistributedTangent(dp, ubar, "tensor4")
-        make_op = lambda s: public.local if s == "tensor4" else MatrixFreeTangent(prob, ubar, s)  # noqa: E731
-    x = torch.from_numpy(x_host).cuda()
-    y = torch.empty_like(x)
+        comm.barrier()
+        cfg5 = _cfg5(comm, args.steps, args.warmup, flush=flush, headline=args)
+        h = cfg5.pop("_headline")
+    prob = h["prob"]
     nqp = prob.mesh.n_elements * prob.n_qpoints_per_cell
-    op = make_op("tensor4")
-    if ws > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with Clocks(torch.cuda.current_device()) as clk:
-        kern_ms, launches = _time_steps(op, x, y, args.steps, args.warmup, flush, flush_l2=False)
-        step_ms = kern_ms
-        if public is not None:
-            step_ms, launches = _time_steps(op, x, y, args.steps, args.warmup, flush, step_fn=public.apply_into,
-                                            flush_l2=False)
-    torch.cuda.synchronize()
-    flushed_ms, _ = _time_steps(op, x, y, max(args.steps // 2, 5), 3, flush)  # transparency: L2 flushed per step
-    if ws > 1:
-        t = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        step_ms, kern_ms = t.tolist()
     ab = algorithmic_bytes("tensor4", 3, prob.n_dofs, nqp)
-    apply_into = public.apply_into if public is not None else op.apply_into
-    e2e_steps = max(args.steps, 200)  # the host link drifts between slow and fast windows: a longer median
-    e2e_ms, h2d, d2h = _e2e(apply_into, x_host, e2e_steps, args.warmup,
-                            public_apply=op.apply if public is None else None)
+    step_ms, kern_ms, e2e_ms = h["step_ms"], h["kern_ms"], h["e2e"]["median"]
     if ws > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([step_ms, kern_ms, e2e_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = t.item()
+        step_ms, kern_ms, e2e_ms = t.tolist()
     traffic = _traffic()
+    n_global = h["n_global"]
+    e2e = {"value": n_global / e2e_ms / 1e6, "unit": "GDoF/s", "h2d_bytes_per_step": h["h2d"],
+           "d2h_bytes_per_step": h["d2h"],
+           "stat": f"median of {h['e2e']['n']} synchronised steps after "
+                   f"{max(args.warmup, E2E_WARMUP_STEPS)} warm-up steps" + (" (max over ranks)" if ws > 1 else ""),
+           "ms": h["e2e"], "mean_GDoF_s": n_global / h["e2e"]["mean"] / 1e6,
+           "p90_GDoF_s": n_global / h["e2e"]["p90"] / 1e6, "pipeline": h.get("pipeline")}
+    if h.get("e2e_ndarray"):
+        nd = h["e2e_ndarray"]
+        e2e["ndarray_apply"] = {"GDoF_s_median": n_global / nd["median"] / 1e6,
+                                "GDoF_s_mean": n_global / nd["mean"] / 1e6, "ms": nd,
+                                "what": "y = MatrixFreeTangent.apply(x) with a pageable numpy x and a fresh "
+                                        "numpy y (the reference signature), host clock per call"}
+    sb = algorithmic_bytes("tensor4", 3, prob.n_dofs, nqp, True)
     line = {"metric": METRIC, "value": n_global / step_ms / 1e6, "unit": "GDoF/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": ("cfg2 3D 32^3 Q2 tensor4 tangent vmult (823,875 DoFs)" if ws == 1 else
-                                    f"cfg2 weak-scaled: 32x32x{32 * ws} Q2 cells, one 32-layer slab per GPU, "
-                                    f"{n_global} DoFs"),
-                       "strategy": "tensor4", "dofs_per_gpu": int(prob.n_dofs),
-                       "l2": "inputs larger than L2: the 262 MB q-point cache exceeds the 126 MB L2 and is "
-                             "streamed from HBM every step (x, y: 13 MB); steps timed back to back",
-                       "ms_per_step_l2_flushed": flushed_ms,
-                       "parallelism": "single GPU" if ws == 1 else f"slab decomposition x{ws} (NCCL interface add)"},
+            "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(ws),
+            "l2_flushed": {"ms_per_step": h["flushed_ms"], "GDoF_s": n_global / h["flushed_ms"] / 1e6 / ws,
+                           "frac": ab / h["flushed_ms"] / 1e6 / hbm,
+                           "note": "rank 0's cell kernel with a 256 MiB L2 flush before each step"},
+            "dofs_per_gpu": int(prob.n_dofs),
             "roofline": {"bound": "hbm", "achieved": ab / kern_ms / 1e6, "peak": hbm, "unit": "GB/s",
                          "frac": ab / kern_ms / 1e6 / hbm, "traffic": traffic["bytes_per_launch"] if traffic else None,
                          "peak_source": peak_kind, "algorithmic_bytes_per_launch": ab,
-                         "algorithmic_bytes_note": "8 (2 N_dof + 36 N_qp): this design's tensor4 cache folds JxW into "
-                                                   "tau and M (SURVEY's P = 37 stores it: "
-                                                   f"{algorithmic_bytes('tensor4', 3, prob.n_dofs, nqp, True)} B)",
-                         "kernel_ms": kern_ms, "kernel": KERNEL},
-            "e2e": {"value": n_global / e2e_ms / 1e6, "unit": "GDoF/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
-                    "stat": f"median of {e2e_steps} synchronised steps after "
-                            f"{max(args.warmup, E2E_WARMUP_STEPS)} warm-up steps",
-                    "pipeline": op.host_info() if public is None and hasattr(op, "host_info") else None},
-            "gpu_launches": launches * args.steps, "clocks": clk.summary()}
+                         "algorithmic_bytes_note": "8 (2 N_dof + 36 N_qp) of one GPU's cells: this design's tensor4 "
+                                                   "cache folds JxW into tau and M (SURVEY's P = 37 stores it: "
+                                                   f"{sb} B)",
+                         "frac_survey_bytes": sb / kern_ms / 1e6 / hbm, "kernel_ms": kern_ms, "kernel": KERNEL},
+            "e2e": e2e, "gpu_launches": h["launches"] * args.steps, "clocks": h["clk"].summary()}
+    if ws > 1:
+        line["cfg5_strong"] = cfg5
     if rank == 0 and ws == 1 and not args.no_extra:
-        line.update(_extras(args, hbm, prob, ubar, x, y, flush, nqp))
+        line.update(_extras(args, hbm, prob, h["ubar"], h["x"], h["y"], flush, nqp))
+    h.clear()
+    del prob
     if not args.no_extra:
-        from paper_1904_13131_b200.distributed import LocalComm
-
-        del op, x, y
-        if public is not None:
-            del public
-        comm5 = TorchComm() if ws > 1 else LocalComm()
-        line["cfg5_strong"] = _cfg5(comm5, 10, 3)
-        if ws > 1 and not args.no_newton:
-            line["newton_slabs"] = _dist_newton(comm5)
+        if ws == 1:
+            line["cfg5_strong"] = _cfg5(LocalComm(), 10, 3)
+        else:
+            line["cfg2_weak"] = _cfg2_weak(args, TorchComm(), flush)
+            if not args.no_newton:
+                line["newton_slabs"] = _dist_newton(TorchComm())
     if rank == 0 and ws == 1 and not args.no_cpu:
-        v, dt, n, _ = cpu_baseline(2, "tensor4", budget_s=20.0, threads=1)
-        line["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": 1, "kind": "port",
-                                "sample": f"oracle numpy port of the reference apply, cfg2 tensor4, {n} applies "
-                                          f"after 1 warm-up ({dt:.2f} s each, 1 BLAS thread)"}
+        from oracle import ref
+
+        v, dt, n, _, kind, what = cpu_baseline(2, "tensor4", budget_s=20.0, threads=1)
+        line["cpu_baseline"] = {"value": v, "unit": "GDoF/s", "cores": 1, "kind": kind,
+                                "sample": f"{what}: {n} applies after 1 warm-up ({dt:.2f} s each), 1 BLAS thread "
+                                          "(the numpy path is single-core: SURVEY P2)",
+                                "cpu_model": ref.cpu_model(), "host_cpus": os.cpu_count()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def _cfg2_weak(args, comm, flush):
+    """Weak scaling: N config-2 cubes stacked along z (32 x 32 x 32N cells), one
+    32-layer slab per GPU; the interface reverse-add is in the timed step."""
+    import torch
+
+    from paper_1904_13131_b200.distributed import DistProblem, DistributedTangent, Slab, slab_ranges
+    from paper_1904_13131_b200.workloads import MATERIAL, host_workload
+
+    ws = comm.size
+    hw = host_workload(2, seed=0, stack=ws)
+    cells = hw.meshes[-1].cells
+    slab = Slab(3, 2, cells, *slab_ranges(cells[-1], ws)[comm.rank])
+    dp = DistProblem(hw.meshes[-1], 2, MATERIAL, slab, comm, hw.masks[-1])
+    op = DistributedTangent(dp, np.ascontiguousarray(slab.local(hw.ubar)), "tensor4")
+    x = torch.from_numpy(np.ascontiguousarray(slab.local(hw.x))).cuda()
+    y = torch.empty_like(x)
+    comm.barrier()
+    step_ms, _ = _time_steps(op.local, x, y, args.steps, args.warmup, flush, step_fn=op.apply_into, flush_l2=False)
+    t = torch.tensor([step_ms], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    step_ms = t.item()
+    n = slab.n_global_dofs
+    return {"workload": f"cfg2 weak-scaled: 32x32x{32 * ws} Q2 cells, one 32-layer slab per GPU, {n} DoFs",
+            "n_gpus": ws, "ms_per_step": step_ms, "GDoF_s": n / step_ms / 1e6,
+            "GDoF_s_per_gpu": n / step_ms / 1e6 / ws}
 
 
 def _extras(args, hbm, prob, ubar, x, y, flush, nqp):
@@ -501,20 +598,36 @@ def _cfg1(cpu: bool):
     if cpu:
         from threadpoolctl import threadpool_limits
 
-        from oracle import hf_oracle as O
+        from oracle import ref
 
         bh = b.cpu().numpy()
         with threadpool_limits(1):
-            oprobs = [O.OProblem(2, 2, p.mesh.cells, p.mesh.vertices, p.mu_el, p.lam_el, p.constraints.mask)
-                      for p in probs]
-            t0 = time.perf_counter()
-            og = O.GMG(oprobs, wl.ubar, "tensor4", 0)
-            ot = O.Tangent(oprobs[-1], wl.ubar, "tensor4")
-            t1 = time.perf_counter()
-            _, its, _ = O.cg(ot.apply, bh, rel_tol=1e-8, preconditioner=og.apply)
-            t2 = time.perf_counter()
+            if ref.available():  # the unmodified reference's own build_gmg + cg
+                hf = ref.hyperfree()
+                rprobs = [ref.problem(hf, 2, p.mesh.cells[0], 2, wl.centres, wl.cfg["radius"], p.constraints.mask)
+                          for p in probs]
+                t0 = time.perf_counter()
+                rg = hf.multigrid.build_gmg(rprobs, wl.ubar, "tensor4", seed=0,
+                                            transfers=hf.multigrid.build_transfers(rprobs))
+                rop = hf.operators.MatrixFreeTangent(rprobs[-1], wl.ubar, "tensor4")
+                t1 = time.perf_counter()
+                _, rrep = hf.solver.cg(rop.apply, bh, rel_tol=1e-8, preconditioner=rg.apply)
+                t2 = time.perf_counter()
+                its, kind, what = rrep.iterations, "reference", "hyperfree (oracle/_ref) build_gmg + cg"
+            else:
+                from oracle import hf_oracle as O
+
+                oprobs = [O.OProblem(2, 2, p.mesh.cells, p.mesh.vertices, p.mu_el, p.lam_el, p.constraints.mask)
+                          for p in probs]
+                t0 = time.perf_counter()
+                og = O.GMG(oprobs, wl.ubar, "tensor4", 0)
+                ot = O.Tangent(oprobs[-1], wl.ubar, "tensor4")
+                t1 = time.perf_counter()
+                _, its, _ = O.cg(ot.apply, bh, rel_tol=1e-8, preconditioner=og.apply)
+                t2 = time.perf_counter()
+                kind, what = "port", "oracle numpy port of build_gmg + cg"
         rec["cpu_port"] = {"gmg_setup_s": t1 - t0, "cg_solve_s": t2 - t1, "cg_iterations": its, "cores": 1,
-                           "kind": "port", "sample": "oracle numpy port of build_gmg + cg at cfg1, one solve"}
+                           "kind": kind, "sample": f"{what} at cfg1, one solve, 1 BLAS thread"}
     return rec
 
 
@@ -552,11 +665,13 @@ def _matrix_based(prob, ubar, x, flush, hbm):
             "note": "cuSPARSE SpMV via torch (library baseline); matrix-free tensor4 apply is the comparison"}
 
 
-def _cfg5(comm, steps: int, warmup: int):
+def _cfg5(comm, steps: int, warmup: int, flush=None, headline=None):
     """Config 5 (128^3 Q2, 50.9M DoFs, 1280 inclusions): tangent vmult and a
     10-iteration GMG-CG on the slab decomposition over all ranks (strong
     scaling: the global problem is fixed), NCCL interface exchange and dot
-    all-reduce timed separately (device events).  Amplitude 0.005 (SPD, H4)."""
+    all-reduce timed separately (device events).  Amplitude 0.005 (SPD, H4).
+    With ``headline`` (the bench args, N > 1) the vmult is also timed as the
+    headline step: kernel-only, L2-flushed and end to end (``_headline``)."""
     import torch
 
     from paper_1904_13131_b200.distributed import CommTimer, build_dist_gmg, dist_cg, level_slabs
@@ -567,7 +682,9 @@ def _cfg5(comm, steps: int, warmup: int):
     fine = hw.meshes[-1]
     sl = level_slabs(3, 2, fine.cells, len(hw.meshes), comm.rank, comm.size)[-1]
     gmg, dp, op = build_dist_gmg(hw.meshes, 2, MATERIAL, hw.masks, np.ascontiguousarray(sl.local(hw.ubar)), comm)
-    x = torch.from_numpy(np.ascontiguousarray(sl.local(hw.x))).cuda()
+    x_host = np.ascontiguousarray(sl.local(hw.x))
+    del hw
+    x = torch.from_numpy(x_host).cuda()
     y = torch.empty_like(x)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
@@ -577,19 +694,36 @@ def _cfg5(comm, steps: int, warmup: int):
     for _ in range(warmup):
         op.apply_into(x, y)
     torch.cuda.synchronize()
+    comm.barrier()
     timer.reset()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        op.apply_into(x, y)
-    e1.record()
-    torch.cuda.synchronize()
+    clk = Clocks(torch.cuda.current_device())
+    with clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            op.apply_into(x, y)
+        e1.record()
+        torch.cuda.synchronize()
     vm_ms = e0.elapsed_time(e1) / steps
     vm_comm = timer.totals_ms()
+    hl = None
+    if headline is not None:
+        from paper_1904_13131_b200.distributed import NO_TIMER
+
+        for lv in gmg.levels:
+            lv.dp.set_timer(NO_TIMER)
+        kern_ms, _ = _time_steps(op.local, x, y, steps, warmup, flush, flush_l2=False)
+        flushed_ms, _ = _time_steps(op.local, x, y, max(steps // 2, 5), 3, flush)
+        e2e, h2d, d2h = _e2e(op.apply_into, x_host, max(steps, 200), warmup)
+        hl = dict(prob=dp.local, n_global=sl.n_global_dofs, step_ms=vm_ms, kern_ms=kern_ms, flushed_ms=flushed_ms,
+                  launches=7, clk=clk, e2e=e2e, h2d=h2d, d2h=d2h)
+        for lv in gmg.levels:
+            lv.dp.set_timer(timer)
     b = y.clone()
     b[dp.mask_dev.bool()] = 0.0
     dist_cg(dp, op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=2)  # warm-up (graph capture)
     torch.cuda.synchronize()
+    comm.barrier()
     timer.reset()
     e0.record()
     _, its, relres, _ = dist_cg(dp, op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=10)
@@ -603,10 +737,15 @@ def _cfg5(comm, steps: int, warmup: int):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     vm_ms, cg_ms, vx, cx, ca = t.tolist()
     n = sl.n_global_dofs
-    return {"workload": "cfg5 128^3 Q2 (50,923,779 DoFs), levels 4..128, strong scaling over slabs",
-            "n_gpus": comm.size, "setup_s": t_setup, "vmult_ms": vm_ms, "vmult_GDoF_s": n / vm_ms / 1e6,
-            "vmult_exchange_ms": vx, "cg10_ms": cg_ms, "cg_iterations": its, "cg_relres_after_10": relres,
-            "cg10_exchange_ms": cx, "cg10_allreduce_ms": ca, "cg10_n_allreduce": cg_comm["n_allreduce"]}
+    out = {"workload": "cfg5 128^3 Q2 (50,923,779 DoFs), levels 4..128, strong scaling over slabs",
+           "n_gpus": comm.size, "setup_s": t_setup, "vmult_ms": vm_ms, "vmult_GDoF_s": n / vm_ms / 1e6,
+           "vmult_exchange_ms": vx, "cg10_ms": cg_ms, "cg_iterations": its, "cg_relres_after_10": relres,
+           "cg10_exchange_ms": cx, "cg10_allreduce_ms": ca, "cg10_n_allreduce": cg_comm["n_allreduce"],
+           "times": "device events on each rank, max over ranks; exchange / all-reduce: event pairs around "
+                    "each NCCL call on its stream, summed"}
+    if hl is not None:
+        out["_headline"] = hl
+    return out
 
 
 def _dist_newton(comm):
@@ -731,6 +870,22 @@ def _newton_iteration(coarse_precision="fp64"):
     return rec
 
 
+def _spawn(n: int) -> int:
+    """``bench.py --gpus N`` without torchrun: start N ranks (one per GPU, NCCL)
+    through torch.distributed.run on this node and return its exit code."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL's INIT lines show the rank count and transport
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -742,10 +897,18 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        run_reference(args)  # rank 0 alone works; no ranks are started for it
+        return
+    if ws == 0 and args.gpus > 1:
+        sys.exit(_spawn(args.gpus))
+    if ws and ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    run_ours(args)
 
 
 if __name__ == "__main__":

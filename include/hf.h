@@ -114,6 +114,13 @@ HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev,
  * diagonal and the element matrices need an fp64 tangent. */
 HF_API int hf_tangent_create_ex(hf_space* sp, int strategy, int storage_bits, const double* ubar_dev, void* stream,
                                 hf_tangent** out, hf_error_info* err);
+/* host-pointer forms for FFI callers holding numpy arrays (the reference-side
+ * ctypes binding of INTEGRATION.md): MatrixFreeTangent(problem, u_bar)
+ * (operators.py:322-326) from a host u_bar, and .diagonal() (395-410) into a
+ * host array; both synchronous */
+HF_API int hf_tangent_create_host(hf_space* sp, int strategy, const double* ubar_host, hf_tangent** out,
+                                  hf_error_info* err);
+HF_API int hf_tangent_diagonal_host(hf_tangent* op, double* d_host);
 /* .apply (331-339): y = A x with zero-in / identity-out constrained handling */
 HF_API int hf_tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, void* stream);
 /* same, but a no-op while *skip_dev != 0 (device-side early exit for graphs) */
@@ -167,6 +174,8 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
  * overlap, 1 graph + serial, 2 direct + overlap, 3 direct + serial, -1 none)
  * and the four measured step times in us (us4[4], 0 if not measured). */
 HF_API int hf_tangent_host_info(const hf_tangent* op, int* variant, float* us4);
+/* wait for the work queued on `stream` (e.g. after hf_tangent_apply_host) */
+HF_API int hf_stream_synchronize(void* stream);
 /* page-lock / release caller-owned host memory (cudaHostRegister) */
 HF_API int hf_host_register(void* host_ptr, long long bytes);
 HF_API int hf_host_unregister(void* host_ptr);

@@ -47,6 +47,8 @@ _SIGS = {
     "hf_jacobian_range": (I, [P, P, P, PD, PD, ct.POINTER(LL), ct.POINTER(I)]),
     "hf_tangent_create": (I, [P, I, P, P, ct.POINTER(P), ct.POINTER(HfErrorInfo)]),
     "hf_tangent_create_ex": (I, [P, I, I, P, P, ct.POINTER(P), ct.POINTER(HfErrorInfo)]),
+    "hf_tangent_create_host": (I, [P, I, P, ct.POINTER(P), ct.POINTER(HfErrorInfo)]),
+    "hf_tangent_diagonal_host": (I, [P, P]),
     "hf_tangent_apply": (I, [P, P, P, P]),
     "hf_tangent_apply_flagged": (I, [P, P, P, P, P]),
     "hf_tangent_apply_raw": (I, [P, P, P, P, P]),
@@ -57,6 +59,7 @@ _SIGS = {
     "hf_tangent_set_alternate": (I, [P, I]),
     "hf_tangent_apply_host": (I, [P, P, P, I, P]),
     "hf_host_register": (I, [P, LL]),
+    "hf_stream_synchronize": (I, [P]),
     "hf_tangent_host_info": (I, [P, ct.POINTER(I), ct.POINTER(ct.c_float)]),
     "hf_host_unregister": (I, [P]),
     "hf_tangent_diagonal": (I, [P, P, P]),

@@ -612,6 +612,24 @@ HF_API int hf_tangent_create(hf_space* sp, int strategy, const double* ubar_dev,
   return hf_tangent_create_ex(sp, strategy, 64, ubar_dev, stream, out, err);
 }
 
+// Host-pointer form for FFI callers that hold numpy arrays (the reference-side
+// ctypes binding): u_bar is staged through a pooled device
+// buffer; synchronous on the default stream.
+HF_API int hf_tangent_create_host(hf_space* sp, int strategy, const double* ubar_host, hf_tangent** out,
+                                  hf_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!sp || !ubar_host || !out) return fail(HF_ERR_ARG, "null argument");
+  double* d = nullptr;
+  HF_CUDA(dmalloc((void**)&d, sizeof(double) * (sp->n_dofs > 0 ? sp->n_dofs : 1)));
+  int rc = HF_OK;
+  if (cudaMemcpy(d, ubar_host, sizeof(double) * sp->n_dofs, cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = fail(HF_ERR_CUDA, "u_bar upload failed");
+  if (rc == HF_OK) rc = hf_tangent_create_ex(sp, strategy, 64, d, nullptr, out, err);
+  cudaDeviceSynchronize();
+  dfree(d);
+  return rc;
+}
+
 static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, const int* skip_dev, int fill,
                          void* stream, long long tile0 = 0, long long tile1 = -1, int reserve_sms = 0) {
   if (!op || !x_dev || !y_dev) return fail(HF_ERR_ARG, "null argument");
@@ -836,6 +854,11 @@ HF_API int hf_tangent_host_info(const hf_tangent* op, int* variant, float* us4) 
   return HF_OK;
 }
 
+HF_API int hf_stream_synchronize(void* stream) {
+  HF_CUDA(cudaStreamSynchronize(S(stream)));
+  return HF_OK;
+}
+
 HF_API int hf_host_register(void* p, long long bytes) {
   if (!p || bytes <= 0) return fail(HF_ERR_ARG, "null or empty host range");
   HF_CUDA(cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault));
@@ -1014,6 +1037,19 @@ HF_API int hf_tangent_diagonal(hf_tangent* op, double* d_dev, void* stream) {
   a.ubar = op->d_ubar;
   HF_CUDA(cell(sp, OP_DIAG, op->strategy, a, s));
   return HF_OK;
+}
+
+HF_API int hf_tangent_diagonal_host(hf_tangent* op, double* d_host) {
+  if (!op || !d_host) return fail(HF_ERR_ARG, "null argument");
+  const long long n = op->sp->n_dofs;
+  double* d = nullptr;
+  HF_CUDA(dmalloc((void**)&d, sizeof(double) * (n > 0 ? n : 1)));
+  int rc = hf_tangent_diagonal(op, d, nullptr);
+  if (rc == HF_OK && cudaMemcpy(d_host, d, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = fail(HF_ERR_CUDA, "diagonal download failed");
+  cudaDeviceSynchronize();
+  dfree(d);
+  return rc;
 }
 
 HF_API int hf_tangent_storage(const hf_tangent* op, long long* storage_bytes, int* payload_scalars,

@@ -465,8 +465,10 @@ class DistributedTangent:
 
     __call__ = apply
 
-    def diagonal(self) -> torch.Tensor:
-        return self.dp.exchange.add(self.local.diagonal())
+    def diagonal_dev(self) -> torch.Tensor:
+        return self.dp.exchange.add(self.local.diagonal_dev())
+
+    diagonal = diagonal_dev
 
 
 def dist_cg(dp: DistProblem, apply_fn, b: torch.Tensor, rel_tol: float = 1e-6, preconditioner=None,
@@ -581,7 +583,7 @@ class DistLevel:
     def __init__(self, dp: DistProblem, u_local, strategy: str, seed: int, level: int):
         self.dp, self.level = dp, level
         self.op = DistributedTangent(dp, u_local, strategy, level=level)
-        self.diag = self.op.diagonal()
+        self.diag = self.op.diagonal_dev()
         self.inv_diag = torch.reciprocal(self.diag)
         self.lam_min, self.lam_max = dist_eigen_range(dp, self.op, self.diag, seed)
         n = dp.n_dofs

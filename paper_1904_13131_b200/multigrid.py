@@ -335,7 +335,7 @@ class LevelOperator:
             self.op = MatrixFreeTangent(problem, u_level, strategy)
         except NonPositiveJacobian as err:
             raise NonPositiveJacobian(f"level {level}: {err}", element=err.element, level=level) from err
-        self.diag = self.op.diagonal()
+        self.diag = self.op.diagonal_dev()
         self.inv_diag = torch.reciprocal(self.diag)
         mask = problem.mask_dev
         if is_coarsest:

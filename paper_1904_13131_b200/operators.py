@@ -292,6 +292,9 @@ class MatrixFreeTangent:
         self.strategy = strategy
         self.storage = storage
         self.dtype = torch.float32 if storage == "fp32" else torch.float64
+        # numpy u_bar -> numpy results from diagonal() (the reference's calling
+        # convention, operators.py:395-410; multigrid.py:226-227 does 1.0 / diag)
+        self._host_io = isinstance(u_bar, np.ndarray)
         ud = dv.as_dev(u_bar)
         h = ct.c_void_p()
         err = HfErrorInfo()
@@ -412,10 +415,18 @@ class MatrixFreeTangent:
         return self.apply(x)
 
     def diagonal(self, as_numpy: bool | None = None):
-        """diag(A), constrained entries 1 (operators.py:395-410); fp64 storage only."""
+        """diag(A), constrained entries 1 (operators.py:395-410); fp64 storage only.
+
+        Returns an ndarray when the tangent was built from an ndarray ``u_bar``
+        (the reference's convention) or ``as_numpy`` is set, else a CUDA tensor."""
+        d = self.diagonal_dev()
+        return d.cpu().numpy() if (self._host_io if as_numpy is None else as_numpy) else d
+
+    def diagonal_dev(self) -> torch.Tensor:
+        """diag(A) as a CUDA fp64 tensor (the form the device-side callers use)."""
         d = torch.empty(self.n_dofs, dtype=torch.float64, device="cuda")
         check(lib().hf_tangent_diagonal(self._op, dv.ptr(d), dv.stream()))
-        return d.cpu().numpy() if as_numpy else d
+        return d
 
     def storage_bytes(self) -> int:
         """Strategy payload plus geometry (operators.py:412-417)."""
@@ -436,6 +447,7 @@ class AssembledTangent:
 
     def __init__(self, problem: Problem, u_bar):
         self.problem = problem
+        self._host_io = isinstance(u_bar, np.ndarray)
         op4 = MatrixFreeTangent(problem, u_bar, "tensor4")  # NonPositiveJacobian propagates
         nel, d = problem.mesh.n_elements, problem.dim
         nld = problem.n_qpoints_per_cell * d
@@ -475,7 +487,11 @@ class AssembledTangent:
 
     __call__ = apply
 
-    def diagonal(self):
+    def diagonal(self, as_numpy: bool | None = None):
+        d = self.diagonal_dev()
+        return d.cpu().numpy() if (self._host_io if as_numpy is None else as_numpy) else d
+
+    def diagonal_dev(self) -> torch.Tensor:
         if self._diag is None:
             m = self.matrix
             crow, col, val = m.crow_indices(), m.col_indices(), m.values()

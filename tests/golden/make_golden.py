@@ -196,6 +196,27 @@ def newton_traction_case():
     print("wrote newton_traction", recs[:, 2].max(), len(recs), flush=True)
 
 
+def newton_bisect_case():
+    """The reference's newton_solve with one load step whose full increment
+    inverts an element: the NonPositiveJacobian path bisects the step once
+    (solver.py:196-199) and reaches the load through the midpoint."""
+    rng = np.random.default_rng(11)
+    centres = rng.random((3, 2))
+    problems = hierarchy_problems(2, (2, 4), 2, centres, 0.2)
+    load = solver.LoadSpec(magnitude=0.6, direction=(0.0, -1.0))
+    res = solver.newton_solve(problems, solver.NewtonSettings(n_load_steps=1), load, "gmg", "tensor4", seed=0)
+    recs = np.array([(r.load_step, r.fraction, r.iteration, r.residual_norm, r.update_norm, r.cg_iterations)
+                     for r in res.records])
+    assert 0.5 in recs[:, 1], "the load step was not bisected"
+    out = dict(centres=centres, radius=0.2, levels_m=np.array((2, 4)), magnitude=0.6, direction=np.array((0.0, -1.0)),
+               n_steps=1, records=recs, u=res.u)
+    for i, p in enumerate(problems):
+        out[f"mu_{i}"] = p.mu_el[:, 0]
+        out[f"lam_{i}"] = p.lam_el[:, 0]
+    np.savez_compressed(os.path.join(HERE, "newton_bisect_2d.npz"), **out)
+    print("wrote newton_bisect", len(recs), flush=True)
+
+
 def newton_prescribed_case(levels_m=(4, 8), n_inc=160, radius=0.04, seed=0, target=-0.05, n_steps=5):
     """Config-4 restatement driven by reference primitives:
     bottom clamp + prescribed top-z displacement, smooth lifting of each load
@@ -272,6 +293,8 @@ def main():
         mg_case("3d_8", 3, (4, 8), 20, 0.08, 0, 0.005, 2)
     if a.only in (None, "newton_t"):
         newton_traction_case()
+    if a.only in (None, "newton_b"):
+        newton_bisect_case()
     if a.newton or a.only == "newton_p":
         newton_prescribed_case()
 

@@ -25,7 +25,7 @@ def test_assembled_tangent_vs_reference(case):
     assert op.strategy == "matrix_based"
     y = op.apply(g["x"])
     assert rel(y, mb["y"]) < 1e-12
-    assert rel(op.diagonal().cpu().numpy(), mb["diag"]) < 1e-12
+    assert rel(op.diagonal(as_numpy=True), mb["diag"]) < 1e-12
     assert op.storage_bytes() == int(mb["storage"])
     assert op.matrix.values().numel() == int(mb["nnz"])
     # the matrix-based and matrix-free tangents are the same operator

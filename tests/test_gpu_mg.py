@@ -116,6 +116,44 @@ def test_newton_traction_reference():
     assert rel(res.u.cpu().numpy(), g["u"]) < 1e-8
 
 
+def test_newton_load_bisection_reference():
+    """One load step whose full increment inverts an element: newton_solve
+    catches NonPositiveJacobian and bisects the step once (solver.py:196-199),
+    keeping the failed attempt's records, as the reference run did."""
+    from paper_1904_13131_b200 import LoadSpec, NewtonSettings, newton_solve
+
+    g = golden("newton_bisect_2d.npz")
+    g["dim"] = 2
+    probs = product_levels(g)
+    res = newton_solve(probs, NewtonSettings(n_load_steps=int(g["n_steps"])),
+                       LoadSpec(float(g["magnitude"]), tuple(g["direction"])), "gmg", "tensor4", seed=0)
+    recs = np.array([(r.load_step, r.fraction, r.iteration, r.residual_norm, r.update_norm, r.cg_iterations)
+                     for r in res.records])
+    ref = g["records"]
+    assert 0.5 in ref[:, 1]
+    assert recs.shape == ref.shape
+    assert np.array_equal(recs[:, :3], ref[:, :3])  # step, fraction (bisected), iteration
+    assert np.all(np.abs(recs[:, 5] - ref[:, 5]) <= 1)
+    big = ref[:, 3] > 1e-9
+    assert np.allclose(recs[big, 3], ref[big, 3], rtol=1e-4)
+    assert rel(res.u.cpu().numpy(), g["u"]) < 1e-8
+
+
+def test_newton_matrix_based_with_gmg():
+    """strategy="matrix_based" with the GMG preconditioner: the fine operator
+    is the assembled CSR, the GMG levels are tensor4 (solver.py:128-135)."""
+    from paper_1904_13131_b200 import LoadSpec, NewtonSettings, newton_solve
+
+    g = golden("newton_traction_2d.npz")
+    g["dim"] = 2
+    probs = product_levels(g)
+    res = newton_solve(probs, NewtonSettings(n_load_steps=int(g["n_steps"])),
+                       LoadSpec(float(g["magnitude"]), tuple(g["direction"])), "gmg", "matrix_based", seed=0)
+    ref = g["records"]
+    assert len(res.records) == len(ref)
+    assert rel(res.u.cpu().numpy(), g["u"]) < 1e-8
+
+
 def test_newton_prescribed_golden():
     """Config-4 restatement (prescribed top displacement) vs the
     golden run driven by reference primitives (tests/golden/make_golden.py)."""
