@@ -164,7 +164,8 @@ def test_residual_is_energy_gradient(name, lib_loaded):
 
 def test_device_pool_reuses_freed_blocks(lib_loaded):
     """A rebuilt tangent takes its cache from the pool (hf_pool_*), and the
-    reused (stale) block gives the same bits as a fresh one."""
+    reused (stale) block gives the same result as a fresh one (up to the
+    order of the fp64 atomic adds, which varies from launch to launch)."""
     import ctypes as ct
 
     from paper_1904_13131_b200 import MatrixFreeTangent
@@ -185,7 +186,7 @@ def test_device_pool_reuses_freed_blocks(lib_loaded):
     op = MatrixFreeTangent(p, g["ubar"], "tensor4")
     pooled2, live2 = info()
     assert pooled2 < pooled and live2 > live
-    assert np.array_equal(op.apply(g["x"]), y0)
+    assert rel(op.apply(g["x"]), y0) < 1e-14
     del op
     assert L.hf_pool_release() == 0
     assert info()[0] == 0
