@@ -51,6 +51,7 @@ template <int N>
 struct TabLine {
   double V[N][N];   // V[l][o]  = N_l(xi_o)
   double Dc[N][N];  // Dc[l][o] = collocation derivative at Gauss point o of Gauss-basis l
+  double D[N][N];   // D[l][o]  = N_l'(xi_o) (the chained kernel, hf_chain.cuh)
   // per-lane packed site offsets of a generated conflict-free layout
   // (LaneMapT::TABLE); read from the constant bank with a per-lane index
   unsigned long long loff[32][2];
@@ -482,9 +483,13 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   // the tile whose data a work slot processes: the range walked forwards, or
   // backwards when a.reverse (slots past the range stay past it)
   auto dtile = [&](long long tl) { return (a.reverse && tl < a.tile1) ? a.tile1 - 1 - (tl - a.tile0) : tl; };
-  // chunk j of this warp: tile tile0 + blockIdx.x + (warp + (j / N) * W) * gridDim.x, iq = j % N
+  // tile of this warp's k-th work item (round robin over blocks and warps)
+  auto tile_k = [&](long long k) -> long long {
+    return dtile(a.tile0 + blockIdx.x + (warp + k * W) * (long long)gridDim.x);
+  };
+  // chunk j of this warp: iq = j % N of its (j / N)-th tile
   auto issue = [&](long long j) {
-    const long long tile = dtile(a.tile0 + blockIdx.x + (warp + (j / N) * W) * (long long)gridDim.x);
+    const long long tile = tile_k(j / N);
     if (tile >= ntiles) return;
     const int s = (int)(j % RW);
     HF_ASSERT(tile * tstride + (j % N + 1) * CH <= a.cache_len);
@@ -516,12 +521,12 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   double* B = bufs[1];  // scratch -> G2 -> queued z part
 
   long long jc = 0;  // this warp's chunk counter
-  const long long tstep = (long long)W * gridDim.x;
   Gather<DIM, N, VAR> nxt;
-  gather_tile<DIM, N, VAR, ST>(a, dtile(a.tile0 + blockIdx.x + (long long)warp * gridDim.x), ntiles, m, t, act, nxt);
-  for (long long tile = a.tile0 + blockIdx.x + (long long)warp * gridDim.x; tile < ntiles; tile += tstep) {
+  gather_tile<DIM, N, VAR, ST>(a, tile_k(0), ntiles, m, t, act, nxt);
+  for (long long k = 0;; ++k) {
+    if (tile_k(k) >= ntiles) break;
     const Gather<DIM, N, VAR> g = nxt;
-    gather_tile<DIM, N, VAR, ST>(a, dtile(tile + tstep), ntiles, m, t, act, nxt);  // in flight during this tile
+    gather_tile<DIM, N, VAR, ST>(a, tile_k(k + 1), ntiles, m, t, act, nxt);  // in flight during this tile
     const long long e = g.e;
     const bool live = g.live;
     double u[DIM][N];

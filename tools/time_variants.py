@@ -27,7 +27,7 @@ for a in sys.argv[1:]:
     if a.startswith("--reps="):
         reps = int(a.split("=", 1)[1])
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-sink = torch.empty(1, dtype=torch.float32, device="cuda")
+sink = torch.empty((), dtype=torch.float32, device="cuda")
 hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                   "MEASURED_PEAKS.json")))["hbm_gbs"]
 
