@@ -278,7 +278,8 @@ def _config(ws: int) -> dict:
             "strategy": "tensor4",
             "l2": "inputs larger than L2: the 16.8 GB q-point cache (2.1-8.4 GB per GPU) is streamed from HBM "
                   "every step; steps timed back to back",
-            "parallelism": f"z-slab cell partition x{ws}, NCCL interface reverse-add + dot all-reduce"}
+            "parallelism": f"Morton (space-filling-curve) cell partition x{ws}, NCCL interface reverse-add + "
+                           "dot all-reduce"}
 
 
 def _ref_apply(cfg_id=2, strategy="tensor4"):
@@ -693,14 +694,18 @@ def _cfg5(comm, steps: int, warmup: int, flush=None, headline=None):
     headline step: kernel-only, L2-flushed and end to end (``_headline``)."""
     import torch
 
-    from paper_1904_13131_b200.distributed import CommTimer, build_dist_gmg, dist_cg, level_slabs
+    from paper_1904_13131_b200.distributed import CommTimer, build_dist_gmg, dist_cg, level_parts
     from paper_1904_13131_b200.workloads import AMP_SOLVE, MATERIAL, host_workload
 
     t_setup = time.perf_counter()
     hw = host_workload(5, seed=0, amp=AMP_SOLVE, levels=True)
     fine = hw.meshes[-1]
-    sl = level_slabs(3, 2, fine.cells, len(hw.meshes), comm.rank, comm.size)[-1]
-    gmg, dp, op = build_dist_gmg(hw.meshes, 2, MATERIAL, hw.masks, np.ascontiguousarray(sl.local(hw.ubar)), comm)
+    # BASELINE config 5: cells partitioned along a space-filling curve (Morton
+    # boxes: z-halves at 2 ranks, quarters at 4, octants at 8)
+    partition = "morton" if comm.size & (comm.size - 1) == 0 else "slab"
+    sl = level_parts(3, 2, fine.cells, len(hw.meshes), comm.rank, comm.size, partition=partition)[-1]
+    gmg, dp, op = build_dist_gmg(hw.meshes, 2, MATERIAL, hw.masks, np.ascontiguousarray(sl.local(hw.ubar)), comm,
+                                 partition=partition)
     x_host = np.ascontiguousarray(sl.local(hw.x))
     del hw
     x = torch.from_numpy(x_host).cuda()
@@ -757,8 +762,8 @@ def _cfg5(comm, steps: int, warmup: int, flush=None, headline=None):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     vm_ms, cg_ms, vx, cx, ca = t.tolist()
     n = sl.n_global_dofs
-    out = {"workload": "cfg5 128^3 Q2 (50,923,779 DoFs), levels 4..128, strong scaling over slabs",
-           "n_gpus": comm.size, "setup_s": t_setup, "vmult_ms": vm_ms, "vmult_GDoF_s": n / vm_ms / 1e6,
+    out = {"workload": "cfg5 128^3 Q2 (50,923,779 DoFs), levels 4..128, strong scaling",
+           "partition": f"{partition} ({comm.size} parts)", "n_gpus": comm.size, "setup_s": t_setup, "vmult_ms": vm_ms, "vmult_GDoF_s": n / vm_ms / 1e6,
            "vmult_exchange_ms": vx, "cg10_ms": cg_ms, "cg_iterations": its, "cg_relres_after_10": relres,
            "cg10_exchange_ms": cx, "cg10_allreduce_ms": ca, "cg10_n_allreduce": cg_comm["n_allreduce"],
            "times": "device events on each rank, max over ranks; exchange / all-reduce: event pairs around "

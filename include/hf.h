@@ -174,6 +174,9 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
  * overlap, 1 graph + serial, 2 direct + overlap, 3 direct + serial, -1 none)
  * and the four measured step times in us (us4[4], 0 if not measured). */
 HF_API int hf_tangent_host_info(const hf_tangent* op, int* variant, float* us4);
+/* diagnostic: per-warp timestamps of the last apply of an instrumented build
+ * (HF_TIMELINE=1 -> libhf_tl.so; HF_ERR_UNSUPPORTED otherwise); n >= 148*16*72 */
+HF_API int hf_timeline_fetch(unsigned long long* host, long long n, int clear);
 /* wait for the work queued on `stream` (e.g. after hf_tangent_apply_host) */
 HF_API int hf_stream_synchronize(void* stream);
 /* page-lock / release caller-owned host memory (cudaHostRegister) */
@@ -315,6 +318,17 @@ HF_API int hf_lanczos_step(hf_ws* w, long long n, double* r, double* z, double* 
 /* diagnostic: blocks x threads threads run 8 independent chains of `iters`
  * DFMAs (16 * iters flops per thread) -- the measured fp64 roofline peak */
 HF_API int hf_probe_dfma(long long iters, int blocks, int threads, double* sink_dev, void* stream);
+/* Box partitions (distributed.py Box; the paper's p4est octants): interface
+ * DoFs shared with one neighbour, listed by local index `idx` (the same global
+ * order on both ranks).  hf_halo_pack: buf[i] = y[idx[i]]; hf_halo_unpack_add:
+ * y[idx[i]] += buf[i] where mask[idx[i]] == 0.  hf_dot_owned: sum of a[i] b[i]
+ * over own[i] != 0 (the DoFs this rank owns), deterministic order. */
+HF_API int hf_halo_pack(long long n, const int* idx, const double* y, double* buf, void* stream);
+HF_API int hf_halo_unpack_add(long long n, const int* idx, double* y, const double* buf, const unsigned char* mask,
+                              void* stream);
+HF_API int hf_dot_owned(hf_ws* w, long long n, const double* a, const double* b, const unsigned char* own,
+                        double* out_dev, void* stream);
+
 /* reverse halo add of a slab interface (multi-GPU; no reference
  * analogue -- the paper's MPI ghost exchange):
  * y[i] += recv[i] where mask[i] == 0 */

@@ -60,6 +60,7 @@ _SIGS = {
     "hf_tangent_apply_host": (I, [P, P, P, I, P]),
     "hf_host_register": (I, [P, LL]),
     "hf_stream_synchronize": (I, [P]),
+    "hf_timeline_fetch": (I, [P, LL, I]),
     "hf_tangent_host_info": (I, [P, ct.POINTER(I), ct.POINTER(ct.c_float)]),
     "hf_host_unregister": (I, [P]),
     "hf_tangent_diagonal": (I, [P, P, P]),
@@ -103,6 +104,9 @@ _SIGS = {
     "hf_dot_f32": (I, [P, LL, P, P, P, P]),
     "hf_resnorm_check_f32": (I, [P, LL, P, P, P, I, I, P, P]),
     "hf_halo_add": (I, [LL, P, P, P, P]),
+    "hf_halo_pack": (I, [LL, P, P, P, P]),
+    "hf_halo_unpack_add": (I, [LL, P, P, P, P, P]),
+    "hf_dot_owned": (I, [P, LL, P, P, P, P, P]),
     "hf_probe_dfma": (I, [LL, I, I, P, P]),
 }
 
@@ -126,6 +130,8 @@ def lib():
                               "(there is no CPU fallback)")
         L = ct.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("HF_LIB") and not hasattr(L, name):
+                continue  # an older A/B build (tests check the in-tree library's exports)
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

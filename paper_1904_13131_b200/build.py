@@ -18,12 +18,15 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 DEBUG = os.environ.get("HF_DEBUG", "0") not in ("", "0")  # device bounds checks -> libhf_debug.so
-OBJ = os.path.join(PKG, "build_obj_debug" if DEBUG else "build_obj")
-LIB = os.path.join(PKG, "libhf_debug.so" if DEBUG else "libhf.so")
+TIMELINE = os.environ.get("HF_TIMELINE", "0") not in ("", "0")  # per-warp apply timeline -> libhf_tl.so
+_SUFFIX = "_debug" if DEBUG else ("_tl" if TIMELINE else "")
+OBJ = os.path.join(PKG, "build_obj" + _SUFFIX)
+LIB = os.path.join(PKG, f"libhf{_SUFFIX}.so")
 SOURCES = ["hf_api.cu", "hf_cells2d.cu", "hf_cells3d.cu", "hf_assemble.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-         "-I", os.path.join(ROOT, "include")] + (["-DHF_DEBUG"] if DEBUG else [])
+         "-I", os.path.join(ROOT, "include")] + (["-DHF_DEBUG"] if DEBUG else []) + \
+        (["-DHF_TIMELINE"] if TIMELINE else [])
 
 
 def _nvcc() -> str:

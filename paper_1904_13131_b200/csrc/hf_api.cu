@@ -854,6 +854,21 @@ HF_API int hf_tangent_host_info(const hf_tangent* op, int* variant, float* us4) 
   return HF_OK;
 }
 
+// Per-warp timeline of the last instrumented apply (HF_TIMELINE builds only)
+HF_API int hf_timeline_fetch(unsigned long long* host, long long n, int clear) {
+#ifdef HF_TIMELINE
+  if (!host || n < (long long)HF_TL_WARPS * HF_TL_SLOTS) return fail(HF_ERR_ARG, "timeline buffer too small");
+  HF_CUDA(cudaDeviceSynchronize());
+  HF_CUDA(hf::timeline_copy_3d(host, clear));
+  return HF_OK;
+#else
+  (void)host;
+  (void)n;
+  (void)clear;
+  return fail(HF_ERR_UNSUPPORTED, "not an HF_TIMELINE build");
+#endif
+}
+
 HF_API int hf_stream_synchronize(void* stream) {
   HF_CUDA(cudaStreamSynchronize(S(stream)));
   return HF_OK;
@@ -1308,6 +1323,31 @@ HF_API int hf_resnorm_check_f32(hf_ws* w, long long n, const float* b, const flo
   k_resnorm_check<float><<<red_blocks(n), RED_THREADS, 0, s>>>(n, b, ax, w->d_partials, w->d_counter, scal, out_idx,
                                                                 target_idx, flag_dev);
   k_scalar<<<1, 32, 0, s>>>(0, scal, out_idx, target_idx, 0.0, flag_dev);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_halo_pack(long long n, const int* idx, const double* y, double* buf, void* stream) {
+  if (n <= 0) return HF_OK;
+  if (!idx || !y || !buf) return fail(HF_ERR_ARG, "null argument");
+  k_pack_idx<<<vec_blocks(n), 256, 0, S(stream)>>>(n, idx, y, buf);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_halo_unpack_add(long long n, const int* idx, double* y, const double* buf, const unsigned char* mask,
+                              void* stream) {
+  if (n <= 0) return HF_OK;
+  if (!idx || !y || !buf || !mask) return fail(HF_ERR_ARG, "null argument");
+  k_unpack_add_idx<<<vec_blocks(n), 256, 0, S(stream)>>>(n, idx, y, buf, mask);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_dot_owned(hf_ws* w, long long n, const double* a, const double* b, const unsigned char* own,
+                        double* out_dev, void* stream) {
+  if (!w || !a || !b || !own || !out_dev) return fail(HF_ERR_ARG, "null argument");
+  k_dot_owned<<<red_blocks(n), RED_THREADS, 0, S(stream)>>>(n, a, b, own, w->d_partials, w->d_counter, out_dev);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }

@@ -23,6 +23,19 @@ cudaError_t launch_geometry(int dim, const HfTables& tab, const HfLattice& lat, 
   return cudaGetLastError();
 }
 
+cudaError_t timeline_copy_3d(unsigned long long* host, int clear) {
+#ifdef HF_TIMELINE
+  cudaError_t e = cudaMemcpyFromSymbol(host, hf_tl_buf, sizeof(unsigned long long) * HF_TL_WARPS * HF_TL_SLOTS);
+  if (e != cudaSuccess || !clear) return e;
+  static unsigned long long zero[HF_TL_WARPS * HF_TL_SLOTS];
+  return cudaMemcpyToSymbol(hf_tl_buf, zero, sizeof(zero));
+#else
+  (void)host;
+  (void)clear;
+  return cudaErrorNotSupported;
+#endif
+}
+
 int cells_per_block(int dim, int n1) {
   int nq = dim == 2 ? n1 * n1 : n1 * n1 * n1;
   return (256 / nq) > 0 ? 256 / nq : 1;

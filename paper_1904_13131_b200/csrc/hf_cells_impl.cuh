@@ -78,6 +78,7 @@ cudaError_t launch_apply_kernel(const CellArgs& c, cudaStream_t s) {
   a.cache_len = c.cache_len;
   a.reverse = c.reverse;
 
+
   const long long all_tiles = (c.lat.n_el + K::CPW - 1) / K::CPW;
   a.tile0 = c.tile1 < 0 ? 0 : c.tile0;
   a.tile1 = c.tile1 < 0 ? all_tiles : (c.tile1 < all_tiles ? c.tile1 : all_tiles);

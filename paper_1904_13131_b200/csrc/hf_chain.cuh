@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(ChainPlan<DIM, N, VAR, ST>::NT, 1)
   const long long ntiles = a.tile1;
   const long long tstride = (long long)N * CH;
   auto dtile = [&](long long tl) { return (a.reverse && tl < a.tile1) ? a.tile1 - 1 - (tl - a.tile0) : tl; };
-  // tile of this warp's k-th work item (round robin over blocks and warps)
+  // tile of this warp's k-th work item
+  // (round robin over blocks and warps; a global or per-SM dynamic schedule
+  // measured slower: DESIGN.md §4.1)
   auto tile_k = [&](long long k) -> long long {
     return dtile(a.tile0 + blockIdx.x + (warp + k * W) * (long long)gridDim.x);
   };
@@ -196,27 +198,27 @@ __global__ void __launch_bounds__(ChainPlan<DIM, N, VAR, ST>::NT, 1)
     mbar_expect_tx(full + s, (unsigned)(CH * sizeof(ST)));
     tma_load_1d(ring + (size_t)s * CH, cache + tile * tstride + (j % N) * CH, (unsigned)(CH * sizeof(ST)), full + s);
   };
+  bool synced = a.fill != 1;
+  if (a.fill == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
+  int slot, m, t;
+  bool act;
+  line_slot<DIM, N>(lane, slot, m, t, act);
+  Gather<DIM, N, VAR> nxt;
+  gather_tile<DIM, N, VAR, ST>(a, tile_k(0), ntiles, m, t, act, nxt);  // before the TMA burst (hf_line.cuh)
   if (lane == 0) {
     for (int s = 0; s < RW; ++s) mbar_init(full + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int j = 0; j < RW; ++j) issue(j);
   }
   __syncwarp();
-  bool synced = a.fill != 1;
-  if (a.fill == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
-
-  int slot, m, t;
-  bool act;
   LineOff<DIM, N> lo;
-  line_map<DIM, N>(lane, T, slot, m, t, act, lo);
+  line_offsets<DIM, N>(lane, T, m, t, lo);
   double* const wb = lbuf + (size_t)warp * NB * Y::BUF;
   double* buf[DIM];
 #pragma unroll
   for (int b = 0; b < DIM; ++b) buf[b] = wb + b * Y::BUF;
 
   long long jc = 0;
-  Gather<DIM, N, VAR> nxt;
-  gather_tile<DIM, N, VAR, ST>(a, tile_k(0), ntiles, m, t, act, nxt);
   for (long long k = 0;; ++k) {
     if (tile_k(k) >= ntiles) break;
     const Gather<DIM, N, VAR> g = nxt;

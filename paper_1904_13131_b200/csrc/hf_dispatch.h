@@ -19,6 +19,12 @@ cudaError_t launch_geometry(int dim, const HfTables& tab, const HfLattice& lat, 
 cudaError_t launch_assemble(int dim, int n1, const CellArgs& a, double* vals, cudaStream_t s);
 cudaError_t launch_cell_dofs(const HfLattice& lat, int dim, int degree, long long* dofs, cudaStream_t s);
 
+// the 3D apply kernels' per-warp timeline (HF_TIMELINE builds, hf_line.cuh):
+// HF_TL_WARPS warps x HF_TL_SLOTS timestamps
+#define HF_TL_WARPS (148 * 16)
+#define HF_TL_SLOTS 72
+cudaError_t timeline_copy_3d(unsigned long long* host, int clear);
+
 // blocks per grid and cells per block of the cell kernels
 int cells_per_block(int dim, int n1);
 

@@ -41,9 +41,34 @@
 // fespace.py:258-288; scatter fespace.py:296-324.
 #pragma once
 #include "hf_cell.cuh"
+#include "hf_dispatch.h"
 #include "hf_lanemap.h"
 
 namespace hf {
+
+// Per-warp timeline of the apply kernel (instrumented build only:
+// HF_TIMELINE=1 python -m paper_1904_13131_b200.build -> libhf_tl.so;
+// hf_timeline_fetch; tools/timeline.py).  Slot 0: kernel entry; per tile k:
+// 1 + 4k tile start, 2 + 4k gradients done, 3 + 4k point phase done, 4 + 4k
+// tile end; the last slot: exit.  %globaltimer, ns.
+#ifdef HF_TIMELINE
+static __device__ unsigned long long hf_tl_buf[HF_TL_WARPS * HF_TL_SLOTS];  // one per translation unit
+HF_DEV unsigned long long hf_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HF_TL(slot)                                                                                   \
+  do {                                                                                                \
+    const int _s = (slot);                                                                            \
+    const unsigned _w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);                          \
+    if ((threadIdx.x & 31) == 0 && _w < HF_TL_WARPS && _s < HF_TL_SLOTS) hf_tl_buf[_w * HF_TL_SLOTS + _s] = hf_gtime(); \
+  } while (0)
+#else
+#define HF_TL(slot) \
+  do {              \
+  } while (0)
+#endif
 
 // 1D tables as a kernel parameter: indexed with compile-time constants only,
 // so they are constant-bank operands.
@@ -139,19 +164,32 @@ struct LineOff {
   int off[DIM][N];
 };
 
-// lane -> (slot = cell * L + line, cell m, line t, active) and its site offsets
+// lane -> (slot = cell * L + line, cell m, line t, active): immediates only,
+// no memory access (the kernel issues its first gather right after)
 template <int DIM, int N>
-HF_DEV void line_map(int lane, const TabLine<N>& T, int& slot, int& m, int& t, bool& act, LineOff<DIM, N>& o) {
+HF_DEV void line_slot(int lane, int& slot, int& m, int& t, bool& act) {
   using K = LineCfg<DIM, N>;
-  using Y = LineLay<DIM, N>;
   if constexpr (LineMap<DIM, N>::CUSTOM) {
     using Z = LaneMapT<DIM, N>;
     const unsigned long long w = lane < 12 ? Z::B0 : (lane < 24 ? Z::B1 : Z::B2);
     const int sl = (int)((w >> (5 * (lane % 12))) & 31ull);
     act = sl != 31;
     slot = act ? sl : 0;
-    m = slot / K::L;
-    t = slot - m * K::L;
+  } else {
+    act = lane < K::LANES;
+    slot = act ? lane : 0;
+  }
+  m = slot / K::L;
+  t = slot - m * K::L;
+}
+
+// the lane's line-buffer site offsets (the generated layout reads a per-lane
+// table from the kernel parameters: a constant-cache miss at kernel start)
+template <int DIM, int N>
+HF_DEV void line_offsets(int lane, const TabLine<N>& T, int m, int t, LineOff<DIM, N>& o) {
+  using Y = LineLay<DIM, N>;
+  if constexpr (LineMap<DIM, N>::CUSTOM) {
+    using Z = LaneMapT<DIM, N>;
     constexpr int per = 64 / Z::OFF_BITS;
     unsigned long long ow[Z::OFF_WORDS];
 #pragma unroll
@@ -160,10 +198,6 @@ HF_DEV void line_map(int lane, const TabLine<N>& T, int& slot, int& m, int& t, b
     for (int k = 0; k < DIM * N; ++k)
       o.off[k / N][k % N] = (int)((ow[k / per] >> (Z::OFF_BITS * (k % per))) & ((1ull << Z::OFF_BITS) - 1));
   } else {
-    act = lane < K::LANES;
-    m = act ? lane / K::L : 0;
-    t = act ? lane - m * K::L : 0;
-    slot = m * K::L + t;
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       o.off[0][l] = (lbase<DIM, N, 0>(t) + l * lstride<DIM, N, 0>()) * Y::CPWP + m;
@@ -472,6 +506,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   constexpr int NV = DIM * (DIM + 1) / 2;
   constexpr int NM = NV * (NV + 1) / 2;
   if (a.skip && *a.skip) return;
+  HF_TL(0);
   extern __shared__ __align__(128) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ST* ring = reinterpret_cast<ST*>(smem) + (size_t)warp * RW * CH;  // this warp's stages (16-byte aligned)
@@ -483,7 +518,9 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   // the tile whose data a work slot processes: the range walked forwards, or
   // backwards when a.reverse (slots past the range stay past it)
   auto dtile = [&](long long tl) { return (a.reverse && tl < a.tile1) ? a.tile1 - 1 - (tl - a.tile0) : tl; };
-  // tile of this warp's k-th work item (round robin over blocks and warps)
+  // tile of this warp's k-th work item
+  // (round robin over blocks and warps; a global or per-SM dynamic schedule
+  // measured slower: DESIGN.md §4.1)
   auto tile_k = [&](long long k) -> long long {
     return dtile(a.tile0 + blockIdx.x + (warp + k * W) * (long long)gridDim.x);
   };
@@ -496,12 +533,6 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     mbar_expect_tx(full + s, (unsigned)(CH * sizeof(ST)));
     tma_load_1d(ring + (size_t)s * CH, cache + tile * tstride + (j % N) * CH, (unsigned)(CH * sizeof(ST)), full + s);
   };
-  if (lane == 0) {
-    for (int s = 0; s < RW; ++s) mbar_init(full + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int j = 0; j < RW; ++j) issue(j);
-  }
-  __syncwarp();
   // y = mask ? x : 0 is written by the preceding k_fill_masked launch.  With
   // programmatic dependent launch (a.fill != 0) this kernel starts while that
   // fill is still running: TMA loads, gathers and the evaluation overlap it,
@@ -509,10 +540,23 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   bool synced = a.fill != 1;
   if (a.fill == 2) asm volatile("griddepcontrol.wait;" ::: "memory");  // x comes from the primary
 
+  // Start-up order: the first tile's gather, then its TMA chunks, then the
+  // constant-bank offsets.  Every warp of the grid starts at once and the TMA
+  // burst (23 KB per warp at config 2) would otherwise queue the 9 gather
+  // loads behind it; the first tile waited ~3 us for them (tools/timeline.py).
   int slot, m, t;
   bool act;
+  line_slot<DIM, N>(lane, slot, m, t, act);
+  Gather<DIM, N, VAR> nxt;
+  gather_tile<DIM, N, VAR, ST>(a, tile_k(0), ntiles, m, t, act, nxt);
+  if (lane == 0) {
+    for (int s = 0; s < RW; ++s) mbar_init(full + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int j = 0; j < RW; ++j) issue(j);
+  }
+  __syncwarp();
   LineOff<DIM, N> lo;
-  line_map<DIM, N>(lane, T, slot, m, t, act, lo);
+  line_offsets<DIM, N>(lane, T, m, t, lo);
   double* wb = lbuf + (size_t)warp * NB * Y::BUF;
   double* bufs[NB];
 #pragma unroll
@@ -521,10 +565,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   double* B = bufs[1];  // scratch -> G2 -> queued z part
 
   long long jc = 0;  // this warp's chunk counter
-  Gather<DIM, N, VAR> nxt;
-  gather_tile<DIM, N, VAR, ST>(a, tile_k(0), ntiles, m, t, act, nxt);
-  for (long long k = 0;; ++k) {
+  long long k = 0;
+  for (;; ++k) {
     if (tile_k(k) >= ntiles) break;
+    HF_TL(1 + 4 * (int)k);
     const Gather<DIM, N, VAR> g = nxt;
     gather_tile<DIM, N, VAR, ST>(a, tile_k(k + 1), ntiles, m, t, act, nxt);  // in flight during this tile
     const long long e = g.e;
@@ -552,6 +596,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       eval_line2<DIM, N>(T, u, g.ub, live, lo, A, B, G1, G2, bufs[NB - 2], bufs[NB - 1], Gx, Gxu);
     else
       eval_line<DIM, N>(T, u, live, lo, A, B, G1, G2, Gx);
+    HF_TL(2 + 4 * (int)k);
 
     // ---------------- P: q-point physics along this thread's x-line ----------------
     double mu = 0.0, lam = 0.0;
@@ -679,6 +724,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       }
     }
     __syncwarp();
+    HF_TL(3 + 4 * (int)k);
     // ---------------- I1: transposed collocation derivative per axis (x in registers, y/z in place) ----------------
     if (live) {
       double v[DIM][N];
@@ -758,7 +804,9 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       }
     }
     __syncwarp();  // line buffers are reused by the next tile
+    HF_TL(4 + 4 * (int)k);
   }
+  HF_TL(HF_TL_SLOTS - 1);
 }
 
 }  // namespace hf

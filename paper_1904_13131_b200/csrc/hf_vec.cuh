@@ -56,6 +56,32 @@ __global__ void k_halo_add(long long n, double* __restrict__ y, const double* __
     if (!mask[i]) y[i] += recv[i];
 }
 
+// interface DoFs of a box partition (distributed.py Box): buf[i] = y[idx[i]]
+// packs the partial sums sent to one neighbour; y[idx[i]] += buf[i] adds a
+// neighbour's partials on the unconstrained DoFs.  Within one neighbour's list
+// every idx is distinct, so the add needs no atomics.
+__global__ void k_pack_idx(long long n, const int* __restrict__ idx, const double* __restrict__ y,
+                           double* __restrict__ buf) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    buf[i] = y[idx[i]];
+}
+__global__ void k_unpack_add_idx(long long n, const int* __restrict__ idx, double* __restrict__ y,
+                                 const double* __restrict__ buf, const unsigned char* __restrict__ mask) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int j = idx[i];
+    if (!mask[j]) y[j] += buf[i];
+  }
+}
+
+// dot product over the DoFs a rank owns (own[i] != 0), deterministic order
+__global__ void k_dot_owned(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                            const unsigned char* __restrict__ own, double* partials, unsigned* counter, double* out) {
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (own[i]) s = fma(a[i], b[i], s);
+  grid_reduce(s, partials, counter, out);
+}
+
 // fp64 throughput probe (the denominator of the fp64 roofline; MEASURED_PEAKS
 // has no fp64 entry): 8 independent DFMA chains per thread
 __global__ void k_probe_dfma(long long iters, double* sink) {

@@ -274,6 +274,27 @@ class Slab:
             raise ValueError("slab does not coarsen 2:1")
         return Slab(self.dim, self.degree, tuple(c // 2 for c in self.cells), self.c0 // 2, self.c1 // 2)
 
+    # --- the part interface shared with Box (DistProblem, DistGMG, DistHierarchy)
+    @property
+    def has_top(self) -> bool:
+        return not self.has_upper
+
+    def sub_mesh(self, global_mesh: Mesh) -> Mesh:
+        return sub_box(global_mesh, self.axis, self.c0, self.c1)
+
+    def put_local(self, full: torch.Tensor, part: torch.Tensor) -> None:
+        full[self.dof_offset:self.dof_offset + self.n_dofs] = part
+
+    def take_local(self, full: torch.Tensor) -> torch.Tensor:
+        return full[self.dof_offset:self.dof_offset + self.n_dofs]
+
+    def put_owned(self, full: torch.Tensor, part: torch.Tensor) -> None:
+        o = self.owned
+        full[self.dof_offset + o.start:self.dof_offset + o.stop] = part[o]
+
+    def make_exchange(self, comm, mask_dev: torch.Tensor):
+        return SlabExchange(self, comm, mask_dev)
+
 
 def level_slabs(dim: int, degree: int, fine_cells: tuple, n_levels: int, rank: int, size: int,
                 min_cells: int = 2) -> list:
@@ -297,6 +318,230 @@ def level_slabs(dim: int, degree: int, fine_cells: tuple, n_levels: int, rank: i
             out.insert(0, None)
     if n_levels > 1:
         out.insert(0, None)  # the coarsest level is always replicated
+    return out
+
+
+def morton_boxes(cells: tuple, size: int) -> list[tuple[tuple, tuple]]:
+    """Cell boxes of a Morton (Z-order) partition into ``size`` = 2^k contiguous
+    chunks of the space-filling curve (the paper's p4est
+    partition).  On a box whose cell counts are divisible the
+    chunks are boxes: the curve's first bisection halves the last axis, the
+    next the one before it, and so on cyclically, so 2 ranks get z-halves, 4
+    get (z, y) quarters and 8 get octants.  Returns [(lo, hi)] in rank (curve)
+    order."""
+    dim = len(cells)
+    if size < 1 or size & (size - 1):
+        raise ValueError(f"a Morton partition needs a power-of-two rank count, got {size}")
+    boxes = [(tuple(0 for _ in cells), tuple(cells))]
+    level = 0
+    while len(boxes) < size:
+        axis = dim - 1 - (level % dim)
+        out = []
+        for lo, hi in boxes:
+            n = hi[axis] - lo[axis]
+            if n < 2 or n % 2:
+                raise ValueError(f"cannot bisect {n} cells along axis {axis}")
+            mid = lo[axis] + n // 2
+            out.append((lo, tuple(mid if a == axis else h for a, h in enumerate(hi))))
+            out.append((tuple(mid if a == axis else l for a, l in enumerate(lo)), hi))
+        boxes = out
+        level += 1
+    return boxes
+
+
+@dataclass(frozen=True)
+class Box:
+    """One rank's box of a level in a general box partition: cells
+    [lo_a, hi_a) on every axis.  ``boxes`` holds every rank's (lo, hi), so the
+    owner and the neighbours of each interface node follow locally.  The rank's
+    vector is its box's node lattice (interface nodes included), a gather of
+    the global vector (``global_dofs``); a node is owned by the lowest rank
+    whose closed box contains it."""
+
+    dim: int
+    degree: int
+    cells: tuple   # global cells per axis
+    rank: int
+    boxes: tuple   # ((lo, hi), ...) of every rank
+
+    @property
+    def lo(self) -> tuple:
+        return self.boxes[self.rank][0]
+
+    @property
+    def hi(self) -> tuple:
+        return self.boxes[self.rank][1]
+
+    @property
+    def local_cells(self) -> tuple:
+        return tuple(h - l for l, h in zip(self.lo, self.hi))
+
+    @property
+    def local_nodes(self) -> tuple:
+        return tuple(c * self.degree + 1 for c in self.local_cells)
+
+    @property
+    def n_dofs(self) -> int:
+        return int(np.prod(self.local_nodes)) * self.dim
+
+    @property
+    def n_global_dofs(self) -> int:
+        return int(np.prod([c * self.degree + 1 for c in self.cells])) * self.dim
+
+    @property
+    def has_top(self) -> bool:
+        """The box holds part of the domain's top face (the traction face)."""
+        return self.hi[-1] == self.cells[-1]
+
+    def _node_grid(self, lo_n, hi_n):
+        """Global node ids of the node box [lo_n, hi_n] (inclusive), x fastest."""
+        gn = [c * self.degree + 1 for c in self.cells]
+        axes = [np.arange(l, h + 1) for l, h in zip(lo_n, hi_n)]
+        strides = np.cumprod([1] + gn[:-1])
+        idx = np.zeros((1,) * self.dim, dtype=np.int64)
+        for a in range(self.dim):
+            shape = [1] * self.dim
+            shape[self.dim - 1 - a] = len(axes[a])
+            idx = idx + (axes[a] * strides[a]).reshape(shape)
+        return idx.reshape(-1)
+
+    def _node_box(self, r: int):
+        lo, hi = self.boxes[r]
+        return tuple(l * self.degree for l in lo), tuple(h * self.degree for h in hi)
+
+    @property
+    def global_dofs(self) -> np.ndarray:
+        """Global DoF of every local DoF (node-blocked, fespace.py:3-8)."""
+        cache = self.__dict__.get("_gd")
+        if cache is None:
+            nodes = self._node_grid(*self._node_box(self.rank))
+            cache = (nodes[:, None] * self.dim + np.arange(self.dim)[None, :]).reshape(-1)
+            object.__setattr__(self, "_gd", cache)
+        return cache
+
+    @property
+    def owned_mask(self) -> np.ndarray:
+        """Local DoFs this rank owns: no lower rank's closed box contains the node."""
+        cache = self.__dict__.get("_own")
+        if cache is None:
+            lo_n, hi_n = self._node_box(self.rank)
+            coords = np.stack(np.meshgrid(*[np.arange(l, h + 1) for l, h in zip(lo_n, hi_n)], indexing="ij"), -1)
+            coords = coords.transpose(tuple(reversed(range(self.dim))) + (self.dim,)).reshape(-1, self.dim)
+            own = np.ones(len(coords), dtype=bool)
+            for r in range(self.rank):
+                rl, rh = self._node_box(r)
+                own &= ~np.all((coords >= np.array(rl)) & (coords <= np.array(rh)), axis=1)
+            cache = np.repeat(own, self.dim)
+            object.__setattr__(self, "_own", cache)
+        return cache
+
+    def shared(self, peer: int):
+        """Local DoF indices of the nodes shared with ``peer`` (ordered by global
+        DoF, the same order on both ranks), or None."""
+        a_lo, a_hi = self._node_box(self.rank)
+        b_lo, b_hi = self._node_box(peer)
+        lo = tuple(max(x, y) for x, y in zip(a_lo, b_lo))
+        hi = tuple(min(x, y) for x, y in zip(a_hi, b_hi))
+        if any(l > h for l, h in zip(lo, hi)):
+            return None
+        ln = self.local_nodes
+        strides = np.cumprod([1] + list(ln[:-1]))
+        axes = [np.arange(l - o, h - o + 1) for l, h, o in zip(lo, hi, a_lo)]
+        idx = np.zeros((1,) * self.dim, dtype=np.int64)
+        for a in range(self.dim):
+            shape = [1] * self.dim
+            shape[self.dim - 1 - a] = len(axes[a])
+            idx = idx + (axes[a] * strides[a]).reshape(shape)
+        nodes = idx.reshape(-1)
+        return (nodes[:, None] * self.dim + np.arange(self.dim)[None, :]).reshape(-1)
+
+    def peers(self) -> dict:
+        out = {}
+        for r in range(len(self.boxes)):
+            if r != self.rank:
+                s = self.shared(r)
+                if s is not None:
+                    out[r] = s
+        return out
+
+    def local(self, v_global):
+        """This rank's part of a global vector (numpy or torch)."""
+        idx = self.global_dofs
+        if isinstance(v_global, torch.Tensor):
+            return v_global[torch.from_numpy(idx).to(v_global.device)]
+        return np.asarray(v_global)[idx]
+
+    def sub_mesh(self, global_mesh: Mesh) -> Mesh:
+        m = global_mesh
+        for a in range(self.dim):  # each axis is cut once, in the global cell numbering
+            m = sub_box(m, a, self.lo[a], self.hi[a])
+        return m
+
+    # --- device views for the coarse bridge (DistGMG) and owned dots
+    def _dev(self, key, fn):
+        d = self.__dict__.setdefault("_devcache", {})
+        if key not in d:
+            d[key] = fn()
+        return d[key]
+
+    def _gidx(self, device):
+        return self._dev(("g", str(device)), lambda: torch.from_numpy(self.global_dofs).to(device))
+
+    def put_local(self, full: torch.Tensor, part: torch.Tensor) -> None:
+        """full[this part's DoFs] = part (zero-padded partial sums of a bridge)."""
+        full[self._gidx(full.device)] = part
+
+    def take_local(self, full: torch.Tensor) -> torch.Tensor:
+        return full[self._gidx(full.device)]
+
+    def put_owned(self, full: torch.Tensor, part: torch.Tensor) -> None:
+        own = self._dev(("o", str(part.device)), lambda: torch.from_numpy(self.owned_mask).to(part.device))
+        full[self._gidx(full.device)[own]] = part[own]
+
+    def make_exchange(self, comm, mask_dev: torch.Tensor):
+        return BoxExchange(self, comm, mask_dev)
+
+    def halved(self) -> "Box":
+        if any(c % 2 for c in self.cells) or any(v % 2 for lo, hi in self.boxes for v in lo + hi):
+            raise ValueError("box partition does not coarsen 2:1")
+        return Box(self.dim, self.degree, tuple(c // 2 for c in self.cells), self.rank,
+                   tuple((tuple(v // 2 for v in lo), tuple(v // 2 for v in hi)) for lo, hi in self.boxes))
+
+    def min_extent(self) -> int:
+        return min(h - l for lo, hi in self.boxes for l, h in zip(lo, hi))
+
+
+def partition_parts(dim: int, degree: int, cells: tuple, rank: int, size: int, partition: str = "slab"):
+    """The finest level's part of ``rank``: a z-slab (``"slab"``) or a Morton box
+    (``"morton"``, power-of-two rank counts; on 2 ranks it is the same z-half)."""
+    if partition == "slab":
+        return Slab(dim, degree, tuple(cells), *slab_ranges(cells[-1], size)[rank])
+    if partition == "morton":
+        return Box(dim, degree, tuple(cells), rank, tuple(morton_boxes(tuple(cells), size)))
+    raise ValueError(f"unknown partition {partition!r}")
+
+
+def level_parts(dim: int, degree: int, fine_cells: tuple, n_levels: int, rank: int, size: int,
+                min_cells: int = 2, partition: str = "slab") -> list:
+    """Parts of rank ``rank`` on every level, coarsest first (``level_slabs`` for
+    either partition).  A level is distributed while every part keeps >=
+    ``min_cells`` cells along every axis it is cut on and the parts nest 2:1;
+    the levels below, and always the coarsest, are replicated (None)."""
+    if partition == "slab":
+        return level_slabs(dim, degree, fine_cells, n_levels, rank, size, min_cells)
+    fine = partition_parts(dim, degree, fine_cells, rank, size, partition)
+    if size > 1 and fine.min_extent() < min(min_cells, min(fine_cells)):
+        raise ValueError("the finest level is too thin to partition")
+    out = [fine]
+    for _ in range(n_levels - 2):
+        cur = out[0]
+        try:
+            nxt = cur.halved() if cur is not None else None
+        except ValueError:
+            nxt = None
+        out.insert(0, nxt if (nxt is not None and nxt.min_extent() >= min_cells) else None)
+    if n_levels > 1:
+        out.insert(0, None)
     return out
 
 
@@ -351,19 +596,74 @@ class SlabExchange:
         return y
 
 
+def _pack_dev(y, idx, buf):
+    check(lib().hf_halo_pack(idx.numel(), dv.ptr(idx), dv.ptr(y), dv.ptr(buf), dv.stream()))
+
+
+def _unpack_add_dev(y, idx, buf, mask):
+    check(lib().hf_halo_unpack_add(idx.numel(), dv.ptr(idx), dv.ptr(y), dv.ptr(buf), dv.ptr(mask), dv.stream()))
+
+
+class BoxExchange:
+    """Reverse add of the interface partial sums of a box partition: every
+    node a rank shares with a neighbour (a face, an edge or a corner of its
+    box) is packed, swapped over the transport (NCCL send/recv), and the
+    neighbour's partials are added on the unconstrained DoFs.  A node shared
+    by k ranks receives k - 1 partials, one per neighbour list.  ``pack_fn`` /
+    ``unpack_fn`` are the libhf kernels; the CPU tests inject their own."""
+
+    def __init__(self, box: "Box", comm, mask_dev: torch.Tensor, pack_fn=_pack_dev, unpack_fn=_unpack_add_dev):
+        self.box, self.comm, self.mask = box, comm, mask_dev
+        self.pack_fn, self.unpack_fn = pack_fn, unpack_fn
+        self.timer = NO_TIMER
+        dev = mask_dev.device
+        self.idx = {p: torch.from_numpy(i.astype(np.int32)).to(dev) for p, i in box.peers().items()}
+        self.send = {p: torch.empty(i.numel(), dtype=torch.float64, device=dev) for p, i in self.idx.items()}
+        self.recv = {p: torch.empty(i.numel(), dtype=torch.float64, device=dev) for p, i in self.idx.items()}
+        self.peers = self.idx
+
+    def start(self, y: torch.Tensor):
+        for p, i in self.idx.items():
+            self.pack_fn(y, i, self.send[p])
+        return self.comm.exchange_start(self.send, self.recv)
+
+    def finish(self, handle, y: torch.Tensor) -> torch.Tensor:
+        handle.wait()
+        for p, i in self.idx.items():
+            self.unpack_fn(y, i, self.recv[p], self.mask)
+        return y
+
+    def add(self, y: torch.Tensor) -> torch.Tensor:
+        if not self.idx:
+            return y
+        with self.timer.span("exchange"):
+            for p, i in self.idx.items():
+                self.pack_fn(y, i, self.send[p])
+            self.comm.exchange(self.send, self.recv)
+            for p, i in self.idx.items():
+                self.unpack_fn(y, i, self.recv[p], self.mask)
+        return y
+
+
 class DistProblem:
     """A rank's slab of one level: the local ``Problem`` plus its partition data."""
 
-    def __init__(self, global_mesh: Mesh, degree: int, mat: Material, slab: Slab, comm, global_mask: np.ndarray,
+    def __init__(self, global_mesh: Mesh, degree: int, mat: Material, slab, comm, global_mask: np.ndarray,
                  basis_nodes: str = "equispaced"):
-        self.slab, self.comm = slab, comm
+        """``slab``: this rank's part, a ``Slab`` or a ``Box`` (``self.part``)."""
+        self.slab = self.part = slab
+        self.comm = comm
         self.global_mesh = global_mesh
-        local_mesh = sub_box(global_mesh, slab.axis, slab.c0, slab.c1)
-        self.local = Problem(local_mesh, degree, mat, basis_nodes=basis_nodes, has_top_face=not slab.has_upper)
+        self.local = Problem(slab.sub_mesh(global_mesh), degree, mat, basis_nodes=basis_nodes,
+                             has_top_face=slab.has_top)
         mask = np.ascontiguousarray(slab.local(global_mask))
         self.local.constraints = ConstraintSet.from_dofs(self.local.n_dofs, np.flatnonzero(mask))
         self.mask_dev = torch.from_numpy(mask.astype(np.uint8)).cuda()
-        self.exchange = SlabExchange(slab, comm, self.mask_dev)
+        self.exchange = slab.make_exchange(comm, self.mask_dev)
+        self.own_dev = None
+        if isinstance(slab, Box):
+            self.own_dev = torch.from_numpy(slab.owned_mask.astype(np.uint8)).cuda()
+            self._unowned = torch.from_numpy(~slab.owned_mask).cuda()
         self.timer = NO_TIMER
 
     def set_timer(self, timer) -> None:
@@ -380,10 +680,24 @@ class DistProblem:
 
     def dot(self, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         """Global dot product: owned DoFs on this rank, all-reduced (2 scalars max per call site)."""
-        o = self.slab.owned
-        dv.dot(a[o], b[o], out)
+        if self.own_dev is None:
+            o = self.slab.owned
+            dv.dot(a[o], b[o], out)
+        else:
+            check(lib().hf_dot_owned(dv.Workspace.get().handle, a.numel(), dv.ptr(a), dv.ptr(b), dv.ptr(self.own_dev),
+                                     dv.ptr(out), dv.stream()))
         with self.timer.span("allreduce"):
             return self.comm.allreduce_(out)
+
+    def zero_unowned_(self, r: torch.Tensor) -> torch.Tensor:
+        """Zero the entries another rank owns (before a restriction, so every
+        shared fine DoF enters the coarse interface sums once)."""
+        if self.own_dev is None:
+            if self.slab.has_lower:
+                r[:self.slab.plane_dofs] = 0.0
+        else:
+            r.masked_fill_(self._unowned, 0.0)
+        return r
 
     def residual(self, u: torch.Tensor, traction=None) -> torch.Tensor:
         """compute_residual (operators.py:205-224) on the slab + interface add."""
@@ -420,8 +734,8 @@ class DistributedTangent:
         tiles hold every cell of the first / last cell layer that touches an
         interface plane, so the planes' partial sums are final after them."""
         sl = self.dp.slab
-        if not (sl.has_lower or sl.has_upper):
-            return None
+        if not isinstance(sl, Slab) or not (sl.has_lower or sl.has_upper):
+            return None  # box partitions: apply, then exchange (no interior/boundary split)
         nt, cpt = self.local.tiles()
         cells = self.dp.local.mesh.cells
         layer = int(np.prod(cells[:-1]))
@@ -631,16 +945,15 @@ class DistGMG:
         Lv.op.apply_into(x, Lv.ax)
         n = b.numel()
         check(lib().hf_resid_masked(n, dv.ptr(Lv.r), dv.ptr(b), dv.ptr(Lv.ax), dv.ptr(Lv.dp.mask_dev), dv.stream()))
-        if Lv.dp.slab.has_lower:  # the rank below owns the shared plane: count it once
-            Lv.r[:Lv.dp.slab.plane_dofs] = 0.0
+        Lv.dp.zero_unowned_(Lv.r)  # a shared DoF enters the restriction once
         if i == 0:
             cs = self.cslab
             self.bridge.restrict_into(Lv.r, self._cpart, mode=1)
             self._cfull.zero_()
-            self._cfull[cs.dof_offset:cs.dof_offset + cs.n_dofs] = self._cpart
+            cs.put_local(self._cfull, self._cpart)
             self.comm.allreduce_(self._cfull)
             self.rep.apply_into(self._cfull, self._xfull)
-            self.bridge.prolong_into(self._xfull[cs.dof_offset:cs.dof_offset + cs.n_dofs], x, mode=2)
+            self.bridge.prolong_into(cs.take_local(self._xfull).contiguous(), x, mode=2)
         else:
             C = self.levels[i - 1]
             self.transfers[i - 1].restrict_into(Lv.r, C.b, mode=1)
@@ -663,11 +976,12 @@ class DistHierarchy:
     Problems and the bridge between them."""
 
     def __init__(self, global_meshes: list, degree: int, mat: Material, global_masks: list, comm,
-                 min_cells: int = 2, fine_dp: "DistProblem | None" = None):
+                 min_cells: int = 2, fine_dp: "DistProblem | None" = None, partition: str = "slab"):
         nlev = len(global_meshes)
         fine = global_meshes[-1]
         self.comm, self.degree, self.nlev = comm, degree, nlev
-        self.slabs = level_slabs(fine.dim, degree, fine.cells, nlev, comm.rank, comm.size, min_cells)
+        self.partition = partition
+        self.slabs = level_parts(fine.dim, degree, fine.cells, nlev, comm.rank, comm.size, min_cells, partition)
         first = next(i for i, s in enumerate(self.slabs) if s is not None)
         if first == 0:
             raise ValueError("the coarsest level must be replicated (min_cells too small for the hierarchy)")
@@ -684,8 +998,7 @@ class DistHierarchy:
         self.rep_transfers = build_transfers(self.rep_probs)
         self.cslab = self.slabs[first].halved()
         cs = self.cslab
-        self.coarse_local = Problem(sub_box(global_meshes[first - 1], cs.axis, cs.c0, cs.c1), degree, mat,
-                                    has_top_face=not cs.has_upper)
+        self.coarse_local = Problem(cs.sub_mesh(global_meshes[first - 1]), degree, mat, has_top_face=cs.has_top)
         cmask = np.ascontiguousarray(cs.local(global_masks[first - 1]))
         self.coarse_local.constraints = ConstraintSet.from_dofs(self.coarse_local.n_dofs, np.flatnonzero(cmask))
         self.bridge = TransferOperator(self.coarse_local, self.dps[first].local)
@@ -711,8 +1024,7 @@ class DistHierarchy:
         check(lib().hf_inject(self.coarse_local._space, dps[first].local._space, dv.ptr(u[first]), dv.ptr(uc_local),
                               int(keep_constrained), dv.stream()))
         ufull = torch.zeros(cs.n_global_dofs, dtype=torch.float64, device="cuda")
-        o = cs.owned
-        ufull[cs.dof_offset + o.start:cs.dof_offset + o.stop] = uc_local[o]
+        cs.put_owned(ufull, uc_local)
         self.comm.allreduce_(ufull)
         rep_levels = build_level_operators(self.rep_probs, ufull, strategy, seed, keep_constrained)
         replicated = GMGPreconditioner(rep_levels, self.rep_transfers)
@@ -722,12 +1034,13 @@ class DistHierarchy:
 
 def build_dist_gmg(global_meshes: list, degree: int, mat: Material, global_masks: list, u_fine_local, comm,
                    strategy: str = "tensor4", seed: int = 0, min_cells: int = 2, keep_constrained: bool = False,
-                   fine_dp: "DistProblem | None" = None):
+                   fine_dp: "DistProblem | None" = None, partition: str = "slab"):
     """Distributed analogue of build_gmg (multigrid.py:372-382).
 
-    ``global_meshes``/``global_masks``: every level, coarsest first.  Returns
+    ``global_meshes``/``global_masks``: every level, coarsest first;
+    ``partition``: "slab" (z-slabs) or "morton" (SFC boxes).  Returns
     (DistGMG, fine DistProblem, fine DistributedTangent)."""
-    h = DistHierarchy(global_meshes, degree, mat, global_masks, comm, min_cells, fine_dp)
+    h = DistHierarchy(global_meshes, degree, mat, global_masks, comm, min_cells, fine_dp, partition)
     gmg, op = h.build_gmg(u_fine_local, strategy, seed, keep_constrained)
     gmg._hierarchy = h
     return gmg, h.fine, op

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--cells", type=int, default=16)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--newton", action="store_true", help="config-4 prescribed-displacement Newton instead")
+    ap.add_argument("--partition", default="slab", choices=["slab", "morton"])
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = local % max(torch.cuda.device_count(), 1)
@@ -55,7 +56,8 @@ def main():
     ubar = torch.from_numpy(wl.ubar).cuda()
     x = torch.from_numpy(wl.x).cuda()
 
-    gmg_d, dp, op_d = build_dist_gmg(wl.meshes, p, MATERIAL, wl.masks, dp_slice(wl.ubar, comm, wl, p), comm)
+    gmg_d, dp, op_d = build_dist_gmg(wl.meshes, p, MATERIAL, wl.masks, dp_slice(wl.ubar, comm, wl, p, args.partition),
+                                     comm, partition=args.partition)
     sl = dp.slab
     res = {"rank": comm.rank, "size": comm.size, "n_global_dofs": int(fine.n_dofs), "n_local_dofs": int(dp.n_dofs)}
 
@@ -115,12 +117,12 @@ def newton_main(args, comm):
         probs.append(pr)
     settings = NewtonSettings(n_load_steps=2)
     single = newton_solve_prescribed(probs, settings, -0.05)
-    h = DistHierarchy(wl.meshes, 2, MATERIAL, wl.masks, comm)
+    h = DistHierarchy(wl.meshes, 2, MATERIAL, wl.masks, comm, partition=args.partition)
     fine = wl.meshes[-1]
     X = node_coordinates(fine, build_dof_map(fine, 2, 3))
     hgt = X[:, 2] / X[:, 2].max()
     sl = h.fine.slab
-    hl = torch.from_numpy(np.ascontiguousarray(hgt[sl.dof_offset // 3:(sl.dof_offset + sl.n_dofs) // 3])).cuda()
+    hl = torch.from_numpy(np.ascontiguousarray(sl.local(np.repeat(hgt, 3))[::3])).cuda()
     u, recs = newton_solve_prescribed_dist(h, settings, -0.05, hl)
     a = np.array([(r.load_step, r.iteration, r.residual_norm, r.cg_iterations) for r in single.records])
     b = np.array([(r.load_step, r.iteration, r.residual_norm, r.cg_iterations) for r in recs])
@@ -136,10 +138,11 @@ def newton_main(args, comm):
     dist.destroy_process_group()
 
 
-def dp_slice(v, comm, wl, p):
-    from paper_1904_13131_b200.distributed import level_slabs
+def dp_slice(v, comm, wl, p, partition="slab"):
+    from paper_1904_13131_b200.distributed import level_parts
 
-    sl = level_slabs(wl.cfg["dim"], p, wl.meshes[-1].cells, len(wl.meshes), comm.rank, comm.size)[-1]
+    sl = level_parts(wl.cfg["dim"], p, wl.meshes[-1].cells, len(wl.meshes), comm.rank, comm.size,
+                     partition=partition)[-1]
     return np.ascontiguousarray(sl.local(v))
 
 

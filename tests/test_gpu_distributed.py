@@ -1,4 +1,4 @@
-"""Slab-decomposed tangent, residual and GMG-CG on the GPU vs the single-GPU
+"""Slab- and Morton-box-decomposed tangent, residual and GMG-CG on the GPU vs the single-GPU
 path (SURVEY §8(e) parity: vmult <= 1e-12 relative, CG iterations +-1).
 
 Ranks are launched with torchrun.  On a one-GPU box they share cuda:0 and
@@ -32,9 +32,10 @@ def _run(nproc, m, backend="gloo", cfg=2, extra=()):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nproc,m", [(2, 16), (4, 16), (3, 12)])
-def test_slab_decomposition_matches_single_gpu(nproc, m):
-    r = _run(nproc, m)
+@pytest.mark.parametrize("nproc,m,partition", [(2, 16, "slab"), (4, 16, "slab"), (3, 12, "slab"),
+                                               (4, 16, "morton"), (8, 16, "morton")])
+def test_decomposition_matches_single_gpu(nproc, m, partition):
+    r = _run(nproc, m, extra=("--partition", partition))
     assert r["size"] == nproc
     for k in ("apply_scalar", "apply_tensor2", "apply_tensor4", "diagonal", "residual"):
         assert r[k] < 1e-12, (k, r[k])
@@ -46,12 +47,13 @@ def test_slab_decomposition_matches_single_gpu(nproc, m):
 
 
 @pytest.mark.gpu
-def test_prescribed_newton_on_slabs_matches_single_gpu():
-    """Config-4 Newton (SURVEY H5 restatement) on 2 slabs vs one GPU: same
-    Newton iterations, CG counts +-1, residual histories, solution."""
+@pytest.mark.parametrize("nproc,partition", [(2, "slab"), (4, "morton")])
+def test_prescribed_newton_on_parts_matches_single_gpu(nproc, partition):
+    """Config-4 Newton (SURVEY H5 restatement) on 2 slabs / 4 Morton boxes vs
+    one GPU: same Newton iterations, CG counts +-1, residual histories, solution."""
     import numpy as np
 
-    r = _run(2, 8, extra=("--newton",))
+    r = _run(nproc, 8, extra=("--newton", "--partition", partition))
     a, b = np.array(r["single"]), np.array(r["dist"])
     assert a.shape == b.shape
     assert np.array_equal(a[:, :2], b[:, :2])

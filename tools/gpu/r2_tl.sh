@@ -1,0 +1,6 @@
+set -x
+cd $GRAFT_REPO_ROOT
+for v in "tensor4 2" "tensor2 2" "scalar 2" "tensor4 3"; do
+  HF_LIB=paper_1904_13131_b200/libhf_tl.so timeout 300 python tools/timeline.py $v
+done
+timeout 300 python tools/time_variants.py 2 --strategies=tensor4,tensor2
