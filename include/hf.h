@@ -166,9 +166,10 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
  * back until the last H2D is done.  On first use per buffer pair all four are
  * timed on this host and the fastest kept (hosts differ: on some, concurrent
  * H2D + D2H is slower than back to back, or a graph with host-memory copy
- * nodes launches slower than direct enqueues).  Each buffer pair is timed
- * once more on its 257th call (a first calibration can land in a slow window
- * of the host link).  The calls that calibrate synchronise `stream`.
+ * nodes launches slower than direct enqueues).  With HF_E2E_RECAL=1 each
+ * buffer pair is timed once more on its 257th call (a first calibration can
+ * land in a slow window of the host link).  The calls that calibrate
+ * synchronise `stream` (a recalibration first waits for the pair's last step).
  * HF_E2E_ORDER=0..3 forces one variant and turns calibration off.
  * hf_tangent_host_info: the variant kept by the last calibration (0 graph +
  * overlap, 1 graph + serial, 2 direct + overlap, 3 direct + serial, -1 none)

@@ -204,9 +204,11 @@ struct HostPipe {
   } g[NG] = {};
   // A first calibration can fall into a window in which the host link runs
   // ~1.7x slow (tens of ms at a time, early in a process on some boxes), and
-  // then picks a variant that is not the fastest in steady state: each entry
-  // is calibrated once more after this many calls.
+  // then picks a variant that is not the fastest in steady state.  With
+  // HF_E2E_RECAL=1 each entry is calibrated once more after this many calls
+  // (opt-in: the recalibration synchronises and stalls the caller's loop).
   static constexpr unsigned RECAL_AT = 256;
+  cudaEvent_t done = nullptr;  // recorded after every enqueued step (any caller stream)
   int ng = 0;
   unsigned long long clock = 0;
   int last_order = -1;           // variant of the last calibration: 0 graph overlap, 1 graph serial,
@@ -729,6 +731,7 @@ static void host_pipe_free(HostPipe* h) {
   for (int i = 0; i < h->ng; ++i)
     if (h->g[i].exec) cudaGraphExecDestroy(h->g[i].exec);
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  if (h->done) cudaEventDestroy(h->done);
   if (h->cap) cudaStreamDestroy(h->cap);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
@@ -905,13 +908,17 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
     HF_CUDA(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
     HF_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
     HF_CUDA(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    HF_CUDA(cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming));
   }
   HostPipe::Entry* hit = nullptr;
   for (int i = 0; i < h->ng; ++i)
     if (h->g[i].x == x_host && h->g[i].y == y_host && h->g[i].chunks == chunks) hit = &h->g[i];
   int recal_slot = -1;
-  if (hit && !hit->recal && hit->uses >= HostPipe::RECAL_AT && !std::getenv("HF_E2E_ORDER")) {
-    HF_CUDA(cudaStreamSynchronize(S(stream)));  // the entry's graph may still be running
+  const bool recal_on = std::getenv("HF_E2E_RECAL") && !std::getenv("HF_E2E_ORDER");
+  if (hit && recal_on && !hit->recal && hit->uses >= HostPipe::RECAL_AT) {
+    hit->recal = 1;  // once, whatever the outcome below
+    // the entry's graph may still run from an earlier call on any stream
+    HF_CUDA(cudaEventSynchronize(h->done));
     if (hit->exec) HF_CUDA(cudaGraphExecDestroy(hit->exec));
     hit->exec = nullptr;
     hit->variant = 2;  // direct enqueue until the recalibration below has finished
@@ -972,18 +979,26 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
           }
           return direct(v == 3);
         };
+        auto drop = [&]() {  // error path: no candidate graph leaks
+          for (int c = 0; c < 2; ++c)
+            if (cand[c]) cudaGraphExecDestroy(cand[c]);
+        };
         int rc = HF_OK;
         for (int w = 0; w < 2 && rc == HF_OK; ++w) rc = run();
-        if (rc != HF_OK) return rc;
-        HF_CUDA(cudaStreamSynchronize(S(stream)));
+        if (rc != HF_OK || cudaStreamSynchronize(S(stream)) != cudaSuccess) {
+          drop();
+          return rc != HF_OK ? rc : fail(HF_ERR_CUDA, "host pipeline calibration failed");
+        }
         // host wall time of one synchronised step (enqueue cost included),
         // best of 5: the host link is noisy
         float us = 1e30f;
         for (int r = 0; r < 5; ++r) {
           const auto t0 = std::chrono::steady_clock::now();
           rc = run();
-          if (rc != HF_OK) return rc;
-          HF_CUDA(cudaStreamSynchronize(S(stream)));
+          if (rc != HF_OK || cudaStreamSynchronize(S(stream)) != cudaSuccess) {
+            drop();
+            return rc != HF_OK ? rc : fail(HF_ERR_CUDA, "host pipeline calibration failed");
+          }
           us = std::min(us, std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - t0).count());
         }
         h->last_us[v] = us;
@@ -1015,9 +1030,12 @@ HF_API int hf_tangent_apply_host(hf_tangent* op, const double* x_host, double* y
   ++hit->uses;
   if (hit->exec) {
     HF_CUDA(cudaGraphLaunch(hit->exec, S(stream)));
-    return HF_OK;
+  } else {
+    const int rc = direct(hit->variant == 3);
+    if (rc != HF_OK) return rc;
   }
-  return direct(hit->variant == 3);
+  HF_CUDA(cudaEventRecord(h->done, S(stream)));
+  return HF_OK;
 }
 
 HF_API int hf_tangent_assemble_local(hf_tangent* op, double* vals_dev, void* stream) {

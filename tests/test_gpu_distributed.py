@@ -62,3 +62,25 @@ def test_prescribed_newton_on_parts_matches_single_gpu(nproc, partition):
     # each Newton step's CG stops at rel 1e-6 (solver.py:85): the two paths' final
     # states agree to the Newton tolerance, not to rounding
     assert r["u_rel"] < 1e-6
+
+
+def _gpus():
+    import torch
+
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nproc,partition", [(2, "slab"), (2, "morton"), (4, "morton"), (8, "morton")])
+def test_nccl_ranks_match_single_gpu(nproc, partition):
+    """One rank per GPU over NCCL (NVLink): the interface exchange through
+    batched send/recv on the device, the dots through ncclAllReduce.  Runs
+    where the box has the GPUs (skipped on a one-GPU box)."""
+    if _gpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs, found {_gpus()}")
+    r = _run(nproc, 16, backend="nccl", extra=("--partition", partition))
+    assert r["size"] == nproc and r["backend"] == "nccl"
+    for k in ("apply_scalar", "apply_tensor2", "apply_tensor4", "diagonal", "residual"):
+        assert r[k] < 1e-12, (k, r[k])
+    assert abs(r["cg_iterations_dist"] - r["cg_iterations_single"]) <= 1, r
+    assert r["cg_solution"] < 1e-5, r

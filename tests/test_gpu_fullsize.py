@@ -272,10 +272,11 @@ def test_host_apply_graph_chunks_and_buffers(cfg, m):
         check(lib().hf_host_unregister(ct.c_void_p(ya.ctypes.data)))
 
 
-def test_host_apply_recalibration():
-    """hf_tangent_apply_host recalibrates each buffer pair's pipeline once
-    after HostPipe::RECAL_AT (256) calls: results stay exact across it and the
-    pipeline info reports a variant afterwards."""
+def test_host_apply_recalibration(monkeypatch):
+    """With HF_E2E_RECAL=1, hf_tangent_apply_host recalibrates each buffer
+    pair's pipeline once after HostPipe::RECAL_AT (256) calls: results stay
+    exact across it and the pipeline info reports a variant afterwards."""
+    monkeypatch.setenv("HF_E2E_RECAL", "1")
     from paper_1904_13131_b200 import MatrixFreeTangent
     from paper_1904_13131_b200.workloads import make_workload
 
