@@ -19,14 +19,16 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 DEBUG = os.environ.get("HF_DEBUG", "0") not in ("", "0")  # device bounds checks -> libhf_debug.so
 TIMELINE = os.environ.get("HF_TIMELINE", "0") not in ("", "0")  # per-warp apply timeline -> libhf_tl.so
-_SUFFIX = "_debug" if DEBUG else ("_tl" if TIMELINE else "")
+# A/B builds: HF_VARIANT_NAME=x HF_VARIANT_FLAGS="-DFOO=1" -> libhf_x.so
+VARIANT = os.environ.get("HF_VARIANT_NAME", "")
+_SUFFIX = "_debug" if DEBUG else ("_tl" if TIMELINE else (f"_{VARIANT}" if VARIANT else ""))
 OBJ = os.path.join(PKG, "build_obj" + _SUFFIX)
 LIB = os.path.join(PKG, f"libhf{_SUFFIX}.so")
 SOURCES = ["hf_api.cu", "hf_cells2d.cu", "hf_cells3d.cu", "hf_assemble.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-I", os.path.join(ROOT, "include")] + (["-DHF_DEBUG"] if DEBUG else []) + \
-        (["-DHF_TIMELINE"] if TIMELINE else [])
+        (["-DHF_TIMELINE"] if TIMELINE else []) + os.environ.get("HF_VARIANT_FLAGS", "").split()
 
 
 def _nvcc() -> str:

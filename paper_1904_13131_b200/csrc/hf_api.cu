@@ -131,9 +131,14 @@ inline unsigned vec_blocks(long long n) {
 
 // the fill: four elements per thread per iteration, one resident wave (148 SMs x 8 blocks of 256)
 inline unsigned fill_blocks(long long n) {
+  static const int per_sm = [] {  // HF_FILL_BLOCKS: A/B knob (blocks of 256 threads per SM)
+    const char* e = std::getenv("HF_FILL_BLOCKS");
+    const int v = e ? std::atoi(e) : 8;
+    return v > 0 ? v : 8;
+  }();
   long long b = (n + 1023) / 1024;
   if (b < 1) b = 1;
-  if (b > 148 * 8) b = 148 * 8;
+  if (b > 148ll * per_sm) b = 148ll * per_sm;
   return (unsigned)b;
 }
 

@@ -486,7 +486,10 @@ struct LinePlan {
   static constexpr int W0 = (int)(BUDGET / perw(RW));
   // warps per block: shared memory bound, capped so the registers of the
   // heaviest variant still fit (scalar ~210 regs -> 8 warps, others ~170 -> 12)
-  static constexpr int WMAX = VAR == SCALAR ? 8 : 12;
+#ifndef HF_SCALAR_WMAX
+#define HF_SCALAR_WMAX 8
+#endif
+  static constexpr int WMAX = VAR == SCALAR ? HF_SCALAR_WMAX : 12;
   static constexpr int W = W0 > WMAX ? WMAX : (W0 < 1 ? 1 : W0);
   static constexpr int NT = 32 * W;
   static constexpr size_t SMEM = (size_t)W * perw(RW);
@@ -549,14 +552,20 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   line_slot<DIM, N>(lane, slot, m, t, act);
   Gather<DIM, N, VAR> nxt;
   gather_tile<DIM, N, VAR, ST>(a, tile_k(0), ntiles, m, t, act, nxt);
+  HF_TL(HF_TL_SLOTS - 4);
   if (lane == 0) {
     for (int s = 0; s < RW; ++s) mbar_init(full + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int j = 0; j < RW; ++j) issue(j);
   }
   __syncwarp();
+  HF_TL(HF_TL_SLOTS - 3);
   LineOff<DIM, N> lo;
   line_offsets<DIM, N>(lane, T, m, t, lo);
+#ifdef HF_TIMELINE
+  if (lo.off[0][0] == 12345) lbuf[0] = 0;  // the timestamp below waits for the offsets
+#endif
+  HF_TL(HF_TL_SLOTS - 2);
   double* wb = lbuf + (size_t)warp * NB * Y::BUF;
   double* bufs[NB];
 #pragma unroll
@@ -590,7 +599,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     // scalar: gradients of x and ubar in one pass (ubar's land in bufs[NB-2]
     // (y) and bufs[NB-1] (z)); above Q4 the doubled line registers spill, so
     // the two fields are evaluated one after the other there
-    constexpr bool FUSED = VAR == SCALAR && N <= 5;
+#ifndef HF_SCALAR_FUSED
+#define HF_SCALAR_FUSED 1
+#endif
+    constexpr bool FUSED = HF_SCALAR_FUSED && VAR == SCALAR && N <= 5;
     if (VAR == SCALAR && !FUSED) eval_line<DIM, N>(T, g.ub, live, lo, A, B, bufs[NB - 2], bufs[NB - 1], Gxu);
     if (FUSED)
       eval_line2<DIM, N>(T, u, g.ub, live, lo, A, B, G1, G2, bufs[NB - 2], bufs[NB - 1], Gx, Gxu);

@@ -45,7 +45,7 @@ t0 = t[:, 0].min()
 t = np.where(t > 0, t - t0, np.nan)
 entry, exit_ = t[:, 0], t[:, SLOTS - 1]
 per = []  # (start, evaluated, point done, end) per tile
-for k in range(17):
+for k in range(16):
     c = t[:, 1 + 4 * k: 5 + 4 * k]
     if c.shape[1] < 4 or np.all(np.isnan(c[:, 0])):
         break
@@ -59,6 +59,9 @@ res = {"strategy": s, "cfg": cfg, "event_ms": ms, "warps": int(used.sum()),
        "span_us": float(np.nanmax(exit_)) / 1e3,
        "entry_us": {"max": float(np.nanmax(entry)) / 1e3, "p50": float(np.nanmedian(entry)) / 1e3},
        "first_tile_start_us_p50": float(np.nanmedian(per[:, 0, 0])) / 1e3,
+       "prologue_us_p50": {"gather_issued": float(np.nanmedian(t[:, SLOTS - 4])) / 1e3,
+                           "tma_issued": float(np.nanmedian(t[:, SLOTS - 3])) / 1e3,
+                           "offsets_loaded": float(np.nanmedian(t[:, SLOTS - 2])) / 1e3},
        "exit_us": {"min": float(np.nanmin(exit_)) / 1e3, "p10": float(np.nanpercentile(exit_, 10)) / 1e3,
                    "p50": float(np.nanmedian(exit_)) / 1e3, "max": float(np.nanmax(exit_)) / 1e3},
        "tiles_per_warp": {"min": int(np.min(np.sum(~np.isnan(dur), 1))), "max": int(np.max(np.sum(~np.isnan(dur), 1)))},
