@@ -230,6 +230,28 @@ def test_pinned_host_apply_pipeline_matches_device_apply():
         assert _rel(y_.cuda(), yd) < 1e-14
 
 
+def test_numpy_apply_repeated_uses_staging():
+    """apply(ndarray) -> fresh ndarray (operators.py:331-339): from the third
+    call the tangent stages through page-locked buffers and the host pipeline;
+    results equal the device apply, x is untouched, y is a fresh array."""
+    from paper_1904_13131_b200 import MatrixFreeTangent
+    from paper_1904_13131_b200.workloads import make_workload
+
+    wl = make_workload(2, seed=4, m=8)
+    op = MatrixFreeTangent(wl.fine, wl.ubar, "tensor4")
+    rng = np.random.default_rng(3)
+    outs = []
+    for k in range(6):
+        x = rng.standard_normal(op.n_dofs)
+        x0 = x.copy()
+        y = op.apply(x)
+        assert isinstance(y, np.ndarray) and np.array_equal(x, x0)
+        yd = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.linalg.norm(y - yd) / np.linalg.norm(yd) < 1e-14, k
+        outs.append(y)
+    assert all(a is not b and not np.shares_memory(a, b) for a, b in zip(outs, outs[1:]))
+
+
 @pytest.mark.parametrize("cfg,m", [(1, None), (2, 6), (3, 3)])
 def test_host_apply_graph_chunks_and_buffers(cfg, m):
     """hf_tangent_apply_host: every slab count (incl. more slabs than cell
