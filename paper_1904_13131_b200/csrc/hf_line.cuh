@@ -302,7 +302,7 @@ HF_DEV void gather_tile(const LineArgs& a, long long tile, long long ntiles, int
 // in buffer g1, the axis-2 derivative (3D) in g2.  a and b are scratch; g1 may
 // be a (the y-derivative then overwrites the values in place, line by line,
 // after the z-lines have read them) and g2 may be b.
-template <int DIM, int N>
+template <int DIM, int N, bool KEEPQ = false>
 HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live, const LineOff<DIM, N>& t,
                       double* a, double* b, double* g1, double* g2, double (&Gx)[DIM][N]) {
   double u[DIM][N];
@@ -328,7 +328,14 @@ HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live
     c_line<DIM, N, false>(T.V, u);
     st_line<DIM, N, 0>(a, t, u);  // Q at Gauss points
 #pragma unroll
-    for (int c = 0; c < DIM; ++c) c1d<N, false>(T.Dc, u[c], Gx[c]);
+    for (int c = 0; c < DIM; ++c) {
+      if constexpr (KEEPQ) {  // the point phase differentiates along x itself
+#pragma unroll
+        for (int l = 0; l < N; ++l) Gx[c][l] = u[c][l];
+      } else {
+        c1d<N, false>(T.Dc, u[c], Gx[c]);
+      }
+    }
   }
   __syncwarp();
   if (DIM == 3) {
@@ -352,7 +359,7 @@ HF_DEV void eval_line(const TabLine<N>& T, const double (&u0)[DIM][N], bool live
 // phase has twice the independent work.  Field 1 uses scratch a, b and writes
 // g1, g2 (g1 may be a); field 2 uses c, d and writes its y-derivative in place
 // in c and its z-derivative in d.
-template <int DIM, int N>
+template <int DIM, int N, bool KEEPQ = false>
 HF_DEV void eval_line2(const TabLine<N>& T, const double (&u0)[DIM][N], const double (&w0)[DIM][N], bool live,
                        const LineOff<DIM, N>& t, double* a, double* b, double* g1, double* g2, double* c, double* d,
                        double (&Gx)[DIM][N], double (&Gw)[DIM][N]) {
@@ -391,8 +398,16 @@ HF_DEV void eval_line2(const TabLine<N>& T, const double (&u0)[DIM][N], const do
     st_line<DIM, N, 0>(c, t, w);
 #pragma unroll
     for (int k = 0; k < DIM; ++k) {
-      c1d<N, false>(T.Dc, u[k], Gx[k]);
-      c1d<N, false>(T.Dc, w[k], Gw[k]);
+      if constexpr (KEEPQ) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+          Gx[k][l] = u[k][l];
+          Gw[k][l] = w[k][l];
+        }
+      } else {
+        c1d<N, false>(T.Dc, u[k], Gx[k]);
+        c1d<N, false>(T.Dc, w[k], Gw[k]);
+      }
     }
   }
   __syncwarp();
@@ -456,6 +471,17 @@ HF_DEV void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned lon
       : "memory");
 }
 
+// x-derivative at Gauss point iq (a loop variable) of the Gauss-point values q
+// of a line: sum_l Dc[l][iq] q[l], the table column read warp-uniformly from
+// the kernel parameters
+template <int N>
+HF_DEV double dc_at(const TabLine<N>& T, const double (&q)[N], int iq) {
+  double s = 0.0;
+#pragma unroll
+  for (int l = 0; l < N; ++l) s = fma(T.Dc[l][iq], q[l], s);
+  return s;
+}
+
 // shared-memory plan of one block of W warps, each with NB line buffers and a
 // private ring of RW cache stages
 template <int DIM, int N, int VAR, typename ST = double>
@@ -505,6 +531,11 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   constexpr int NB = PL::NB;
   constexpr int W = PL::W;
   constexpr int RW = PL::RW;
+  // rolled point loop (see below): tensor4 only -- at Q4 it made tensor4 10 %
+  // faster (3,528 -> 2,352 instructions, 45.8 -> 41.4 us at config 3) and
+  // tensor2 / scalar 4-5 % slower (their point phases are cheap, the per-point
+  // x-derivative is not)
+  constexpr bool ROLL = RW < N && VAR == TENSOR4;
   constexpr long long CH = PL::CH;
   constexpr int NV = DIM * (DIM + 1) / 2;
   constexpr int NM = NV * (NV + 1) / 2;
@@ -602,12 +633,16 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 #ifndef HF_SCALAR_FUSED
 #define HF_SCALAR_FUSED 1
 #endif
+    // the point loop runs rolled when the ring does not hold a whole tile; the
+    // x-line owner then keeps its values at the Gauss points and differentiates
+    // them point by point (dc_at) instead of holding all N x-derivatives
+    static_assert(!ROLL || !LineMap<DIM, N>::CUSTOM, "rolled point loop needs the padded layout");
     constexpr bool FUSED = HF_SCALAR_FUSED && VAR == SCALAR && N <= 5;
-    if (VAR == SCALAR && !FUSED) eval_line<DIM, N>(T, g.ub, live, lo, A, B, bufs[NB - 2], bufs[NB - 1], Gxu);
+    if (VAR == SCALAR && !FUSED) eval_line<DIM, N, ROLL>(T, g.ub, live, lo, A, B, bufs[NB - 2], bufs[NB - 1], Gxu);
     if (FUSED)
-      eval_line2<DIM, N>(T, u, g.ub, live, lo, A, B, G1, G2, bufs[NB - 2], bufs[NB - 1], Gx, Gxu);
+      eval_line2<DIM, N, ROLL>(T, u, g.ub, live, lo, A, B, G1, G2, bufs[NB - 2], bufs[NB - 1], Gx, Gxu);
     else
-      eval_line<DIM, N>(T, u, live, lo, A, B, G1, G2, Gx);
+      eval_line<DIM, N, ROLL>(T, u, live, lo, A, B, G1, G2, Gx);
     HF_TL(2 + 4 * (int)k);
 
     // ---------------- P: q-point physics along this thread's x-line ----------------
@@ -619,14 +654,16 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     // one Gauss point of this thread's x-line from its cache chunk
     auto point = [&](const int iq, const ST* st) {
       if (live) {
-      const int pt = lo.off[0][iq];  // this thread's x-line site iq
+      // this thread's x-line site iq (ROLL: iq is a loop variable; the padded
+      // layout puts the sites of an x-line CPWP doubles apart)
+      const int pt = ROLL ? lo.off[0][0] + iq * LineLay<DIM, N>::CPWP : lo.off[0][iq];
       double f[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q) f[q] = (double)st[q * K::LANES];
       double gu[DIM][DIM];
 #pragma unroll
       for (int cc = 0; cc < DIM; ++cc) {
-        gu[cc][0] = Gx[cc][iq];
+        gu[cc][0] = ROLL ? dc_at(T, Gx[cc], iq) : Gx[cc][iq];
         gu[cc][1] = G1[cc * Y::CS + pt];
         if (DIM == 3) gu[cc][DIM - 1] = G2[cc * Y::CS + pt];
       }
@@ -661,7 +698,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
         double gub[DIM][DIM];
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc) {
-          gub[cc][0] = Gxu[cc][iq];
+          gub[cc][0] = ROLL ? dc_at(T, Gxu[cc], iq) : Gxu[cc][iq];
           gub[cc][1] = bufs[NB - 2][cc * Y::CS + pt];
           if (DIM == 3) gub[cc][DIM - 1] = bufs[NB - 1][cc * Y::CS + pt];
         }
@@ -723,7 +760,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       }
       jc += N;
     } else {
-#pragma unroll
+      // Q4 (N = 5 > RW): tensor4's point phase as a rolled loop; five unrolled
+      // copies of its point code made the kernel 3,500 instructions long and
+      // 12 % of the warp stalls were instruction fetches
+#pragma unroll(ROLL ? 1 : N)
       for (int iq = 0; iq < N; ++iq, ++jc) {
         const int s = (int)(jc % RW);
         mbar_wait(full + s, (unsigned)((jc / RW) & 1));
