@@ -1,10 +1,7 @@
 // Instantiation/dispatch of the cell kernels for one dimension.
 #pragma once
 #include "hf_dispatch.h"
-#include "hf_chain.cuh"
 #include "hf_line.cuh"
-#include <cstdlib>
-#include <cstring>
 
 
 namespace hf {
@@ -21,42 +18,17 @@ inline int nsm_cached() {
 
 // Launch of the line-parallel apply (hf_line.cuh): persistent warps, grid
 // sized to the resident capacity (148 SMs x blocks per SM) or the tile count.
-// The apply kernel family: the chained-contraction kernel (hf_chain.cuh) or the
-// collocation kernel (hf_line.cuh).  HF_APPLY=line|chain overrides the default.
-template <int DIM, int N, int VAR>
-inline bool use_chain() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = std::getenv("HF_APPLY");
-    if (e && !std::strcmp(e, "line")) v = 0;
-    else if (e && !std::strcmp(e, "chain")) v = 1;
-    else v = 0;
-  }
-  return v == 1;
-}
-
-template <int DIM, int N, int VAR, typename ST, bool CHAIN>
-struct ApplyKernel {
-  using PL = LinePlan<DIM, N, VAR, ST>;
-  static constexpr auto fn = k_apply_line<DIM, N, VAR, ST>;
-};
 template <int DIM, int N, int VAR, typename ST>
-struct ApplyKernel<DIM, N, VAR, ST, true> {
-  using PL = ChainPlan<DIM, N, VAR, ST>;
-  static constexpr auto fn = k_apply_chain<DIM, N, VAR, ST>;
-};
-
-template <int DIM, int N, int VAR, typename ST, bool CHAIN>
-cudaError_t launch_apply_kernel(const CellArgs& c, cudaStream_t s) {
+cudaError_t launch_apply_line_t(const CellArgs& c, cudaStream_t s) {
   using K = LineCfg<DIM, N>;
-  using AK = ApplyKernel<DIM, N, VAR, ST, CHAIN>;
-  using PL = typename AK::PL;
+  using PL = LinePlan<DIM, N, VAR, ST>;
+  constexpr auto kern = k_apply_line<DIM, N, VAR, ST>;
   static int resident = -1;
   if (resident < 0) {
-    cudaError_t e = cudaFuncSetAttribute(AK::fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::SMEM);
     if (e != cudaSuccess) return e;
     int per_sm = 0, dev = 0, nsm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, AK::fn, PL::NT, PL::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PL::NT, PL::SMEM);
     if (e != cudaSuccess) return e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -87,7 +59,6 @@ cudaError_t launch_apply_kernel(const CellArgs& c, cudaStream_t s) {
     for (int o = 0; o < N; ++o) {
       T.V[l][o] = c.tab.V[l * N + o];
       T.Dc[l][o] = c.tab.Dc[l * N + o];
-      T.D[l][o] = c.tab.D[l * N + o];
     }
   if constexpr (LaneMapT<DIM, N>::ENABLED) {
     using Z = LaneMapT<DIM, N>;
@@ -105,7 +76,7 @@ cudaError_t launch_apply_kernel(const CellArgs& c, cudaStream_t s) {
   if (nb > cap) nb = cap;
   if (nb <= 0) return cudaSuccess;
   if (!c.fill) {
-    AK::fn<<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);
+    kern<<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);
     return cudaGetLastError();
   }
   // programmatic dependent launch after the fill kernel (hf_api.cu)
@@ -119,22 +90,7 @@ cudaError_t launch_apply_kernel(const CellArgs& c, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, AK::fn, a, T);
-}
-
-// (dim, n1) with a chained kernel: the gradients of a line (DIM * DIM * N
-// doubles) stay in registers without spilling up to these sizes
-template <int DIM, int N>
-struct HasChain {
-  static constexpr bool value = (DIM == 3 && N <= 3) || (DIM == 2 && N <= 4);
-};
-
-template <int DIM, int N, int VAR, typename ST>
-cudaError_t launch_apply_line_t(const CellArgs& c, cudaStream_t s) {
-  if constexpr (HasChain<DIM, N>::value) {
-    if (use_chain<DIM, N, VAR>()) return launch_apply_kernel<DIM, N, VAR, ST, true>(c, s);
-  }
-  return launch_apply_kernel<DIM, N, VAR, ST, false>(c, s);
+  return cudaLaunchKernelEx(&cfg, kern, a, T);
 }
 
 template <int DIM, int N, int VAR>

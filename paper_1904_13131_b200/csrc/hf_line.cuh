@@ -76,7 +76,6 @@ template <int N>
 struct TabLine {
   double V[N][N];   // V[l][o]  = N_l(xi_o)
   double Dc[N][N];  // Dc[l][o] = collocation derivative at Gauss point o of Gauss-basis l
-  double D[N][N];   // D[l][o]  = N_l'(xi_o) (the chained kernel, hf_chain.cuh)
   // per-lane packed site offsets of a generated conflict-free layout
   // (LaneMapT::TABLE); read from the constant bank with a per-lane index
   unsigned long long loff[32][2];
@@ -512,10 +511,7 @@ struct LinePlan {
   static constexpr int W0 = (int)(BUDGET / perw(RW));
   // warps per block: shared memory bound, capped so the registers of the
   // heaviest variant still fit (scalar ~210 regs -> 8 warps, others ~170 -> 12)
-#ifndef HF_SCALAR_WMAX
-#define HF_SCALAR_WMAX 8
-#endif
-  static constexpr int WMAX = VAR == SCALAR ? HF_SCALAR_WMAX : 12;
+  static constexpr int WMAX = VAR == SCALAR ? 8 : 12;
   static constexpr int W = W0 > WMAX ? WMAX : (W0 < 1 ? 1 : W0);
   static constexpr int NT = 32 * W;
   static constexpr size_t SMEM = (size_t)W * perw(RW);
@@ -630,14 +626,11 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     // scalar: gradients of x and ubar in one pass (ubar's land in bufs[NB-2]
     // (y) and bufs[NB-1] (z)); above Q4 the doubled line registers spill, so
     // the two fields are evaluated one after the other there
-#ifndef HF_SCALAR_FUSED
-#define HF_SCALAR_FUSED 1
-#endif
     // the point loop runs rolled when the ring does not hold a whole tile; the
     // x-line owner then keeps its values at the Gauss points and differentiates
     // them point by point (dc_at) instead of holding all N x-derivatives
     static_assert(!ROLL || !LineMap<DIM, N>::CUSTOM, "rolled point loop needs the padded layout");
-    constexpr bool FUSED = HF_SCALAR_FUSED && VAR == SCALAR && N <= 5;
+    constexpr bool FUSED = VAR == SCALAR && N <= 5;
     if (VAR == SCALAR && !FUSED) eval_line<DIM, N, ROLL>(T, g.ub, live, lo, A, B, bufs[NB - 2], bufs[NB - 1], Gxu);
     if (FUSED)
       eval_line2<DIM, N, ROLL>(T, u, g.ub, live, lo, A, B, G1, G2, bufs[NB - 2], bufs[NB - 1], Gx, Gxu);
