@@ -746,28 +746,39 @@ def _cfg5(comm, steps: int, warmup: int, flush=None, headline=None):
         op.apply_into(x, y)  # the kernel-only timings left y without the interface add
     b = y.clone()
     b[dp.mask_dev.bool()] = 0.0
-    dist_cg(dp, op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=2)  # warm-up (graph capture)
-    torch.cuda.synchronize()
-    comm.barrier()
-    timer.reset()
-    e0.record()
-    _, its, relres, _ = dist_cg(dp, op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=10)
-    e1.record()
-    torch.cuda.synchronize()
-    cg_ms = e0.elapsed_time(e1)
-    cg_comm = timer.totals_ms()
-    t = torch.tensor([vm_ms, cg_ms, vm_comm["exchange"] / steps, cg_comm["exchange"], cg_comm["allreduce"]],
-                     dtype=torch.float64, device="cuda")
+    from paper_1904_13131_b200.distributed import NO_TIMER
+
+    def cg10(timed_comm):
+        for lv in gmg.levels:
+            lv.dp.set_timer(timer if timed_comm else NO_TIMER)
+        dist_cg(dp, op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=2)  # warm-up (V-cycle graph capture)
+        torch.cuda.synchronize()
+        comm.barrier()
+        timer.reset()
+        e0.record()
+        res = dist_cg(dp, op, b, rel_tol=0.0, preconditioner=gmg, max_iterations=10)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), res, timer.totals_ms()
+
+    # with the communication timed call by call (eager V-cycles), then as run:
+    # over NCCL the V-cycle is one CUDA graph with the NCCL calls inside
+    cg_ms_timed, _, cg_comm = cg10(True)
+    cg_ms, (_, its, relres, _), _ = cg10(False)
+    t = torch.tensor([vm_ms, cg_ms, vm_comm["exchange"] / steps, cg_comm["exchange"], cg_comm["allreduce"],
+                      cg_ms_timed], dtype=torch.float64, device="cuda")
     if comm.size > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    vm_ms, cg_ms, vx, cx, ca = t.tolist()
+    vm_ms, cg_ms, vx, cx, ca, cg_ms_timed = t.tolist()
     n = sl.n_global_dofs
     out = {"workload": "cfg5 128^3 Q2 (50,923,779 DoFs), levels 4..128, strong scaling",
            "partition": f"{partition} ({comm.size} parts)", "n_gpus": comm.size, "setup_s": t_setup, "vmult_ms": vm_ms, "vmult_GDoF_s": n / vm_ms / 1e6,
            "vmult_exchange_ms": vx, "cg10_ms": cg_ms, "cg_iterations": its, "cg_relres_after_10": relres,
-           "cg10_exchange_ms": cx, "cg10_allreduce_ms": ca, "cg10_n_allreduce": cg_comm["n_allreduce"],
+           "cg10_ms_comm_timed": cg_ms_timed, "cg10_exchange_ms": cx, "cg10_allreduce_ms": ca,
+           "cg10_n_allreduce": cg_comm["n_allreduce"],
+           "v_cycle_graph": bool(gmg._graph) if comm.size > 1 else None,
            "times": "device events on each rank, max over ranks; exchange / all-reduce: event pairs around "
-                    "each NCCL call on its stream, summed"}
+                    "each NCCL call on its stream, summed, in a second run with eager V-cycles (cg10_ms_comm_timed)"}
     if hl is not None:
         out["_headline"] = hl
     return out

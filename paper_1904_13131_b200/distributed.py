@@ -933,6 +933,8 @@ class DistGMG:
         self.levels, self.transfers = dist_levels, transfers
         self.bridge, self.rep, self.cslab, self.comm = bridge, replicated, coarse_slab, comm
         self.steps, self.settings = smoothing_steps, settings
+        self._graph = None  # None: not tried yet; False: eager
+        self.graph_error = None
         if replicated is not None:
             n = coarse_slab.n_global_dofs
             self._cfull = torch.zeros(n, dtype=torch.float64, device="cuda")
@@ -963,10 +965,48 @@ class DistGMG:
         Lv.smooth_into(b, x, self.steps, self.settings, x_zero=False)
         return x
 
-    def apply_into(self, b: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    def _eager(self, b: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         top = len(self.levels) - 1
         out.zero_()
         return self._vc(top, b, out)
+
+    def _graph_wanted(self) -> bool:
+        """Replay the V-cycle as one CUDA graph with the NCCL calls inside
+        (NCCL supports stream capture; the host-staged gloo transport does not).
+        Off while a CommTimer is attached (its events time each call eagerly)
+        and with HF_DIST_GRAPH=0."""
+        if os.environ.get("HF_DIST_GRAPH", "1") == "0" or getattr(self.comm, "staged", True):
+            return False
+        return all(lv.dp.timer is NO_TIMER for lv in self.levels)
+
+    def apply_into(self, b: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        if self._graph is False or not self._graph_wanted():
+            return self._eager(b, out)
+        if self._graph is None:
+            self._bs, self._xs = torch.empty_like(b), torch.empty_like(out)
+            self._bs.copy_(b)
+            self._eager(self._bs, self._xs)  # warm-up: communicators, the replicated levels' own graph
+            graph, ok = None, 1.0
+            rep_graph = self.rep.use_graph if self.rep is not None else None
+            if self.rep is not None:
+                self.rep.use_graph = False  # its launches go into this graph (a replay cannot be captured)
+            try:
+                graph = dv.capture_graph(lambda: self._eager(self._bs, self._xs))
+            except Exception as e:  # the transport refused capture: every rank falls back together
+                graph, ok = None, 0.0
+                self.graph_error = f"{type(e).__name__}: {e}"
+            finally:
+                if self.rep is not None:
+                    self.rep.use_graph = rep_graph
+            flag = torch.tensor([ok], dtype=torch.float64, device=b.device)
+            self.comm.allreduce_(flag)
+            self._graph = graph if flag.item() == self.comm.size else False
+            if self._graph is False:
+                return self._eager(b, out)
+        self._bs.copy_(b)
+        self._graph.replay()
+        out.copy_(self._xs)
+        return out
 
 
 class DistHierarchy:

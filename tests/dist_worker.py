@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--newton", action="store_true", help="config-4 prescribed-displacement Newton instead")
     ap.add_argument("--partition", default="slab", choices=["slab", "morton"])
+    ap.add_argument("--graph-check", action="store_true", help="captured vs eager distributed V-cycle")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev = local % max(torch.cuda.device_count(), 1)
@@ -45,6 +46,8 @@ def main():
     comm = TorchComm()
     if args.newton:
         return newton_main(args, comm)
+    if args.graph_check:
+        return graph_main(args, comm)
     wl = host_workload(args.config, seed=0, amp=AMP_SOLVE, levels=True, m=args.cells)
     p = wl.cfg["degree"]
     probs = []
@@ -133,6 +136,35 @@ def newton_main(args, comm):
     if comm.size > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     out["u_rel"] = t.item()
+    if comm.rank == 0:
+        print("DISTRESULT " + json.dumps(out), flush=True)
+    dist.destroy_process_group()
+
+
+def graph_main(args, comm):
+    """The distributed V-cycle replayed as a CUDA graph (NCCL calls inside) vs the
+    same V-cycle run eagerly: identical preconditioned vectors and CG history."""
+    from paper_1904_13131_b200.distributed import build_dist_gmg, dist_cg
+    from paper_1904_13131_b200.workloads import AMP_SOLVE, MATERIAL, host_workload
+
+    wl = host_workload(args.config, seed=0, amp=AMP_SOLVE, levels=True, m=args.cells)
+    p = wl.cfg["degree"]
+    u = dp_slice(wl.ubar, comm, wl, p, args.partition)
+    gmg, dp, op = build_dist_gmg(wl.meshes, p, MATERIAL, wl.masks, u, comm, partition=args.partition)
+    b = torch.from_numpy(np.ascontiguousarray(dp.slab.local(wl.x))).cuda()
+    b[dp.mask_dev.bool()] = 0.0
+    ze, zg = torch.empty_like(b), torch.empty_like(b)
+    gmg._graph = False  # eager
+    gmg.apply_into(b, ze)
+    _, it_e, _, _ = dist_cg(dp, op, b, rel_tol=1e-8, preconditioner=gmg)
+    gmg._graph = None  # capture on the next call
+    diffs = []
+    for _ in range(3):  # first call captures, later calls replay
+        gmg.apply_into(b, zg)
+        diffs.append(float(torch.linalg.norm(zg - ze) / torch.linalg.norm(ze)))
+    _, it_g, _, _ = dist_cg(dp, op, b, rel_tol=1e-8, preconditioner=gmg)
+    out = dict(size=comm.size, backend=args.backend, graph=gmg._graph not in (None, False), diffs=diffs,
+               cg_eager=it_e, cg_graph=it_g, error=gmg.graph_error)
     if comm.rank == 0:
         print("DISTRESULT " + json.dumps(out), flush=True)
     dist.destroy_process_group()

@@ -84,3 +84,16 @@ def test_nccl_ranks_match_single_gpu(nproc, partition):
         assert r[k] < 1e-12, (k, r[k])
     assert abs(r["cg_iterations_dist"] - r["cg_iterations_single"]) <= 1, r
     assert r["cg_solution"] < 1e-5, r
+
+
+@pytest.mark.gpu
+def test_distributed_vcycle_graph_with_nccl():
+    """The distributed V-cycle captured as one CUDA graph with its NCCL calls
+    inside (here one rank: the coarse bridge's ncclAllReduce is captured; with
+    more GPUs the interface send/recv too) equals the eager V-cycle, and
+    GMG-CG takes the same iterations."""
+    nproc = max(1, min(_gpus(), 2))
+    r = _run(nproc, 8, backend="nccl", extra=("--partition", "morton", "--graph-check"))
+    assert r["graph"], r.get("error")
+    assert max(r["diffs"]) < 1e-13, r
+    assert abs(r["cg_graph"] - r["cg_eager"]) <= 1, r
