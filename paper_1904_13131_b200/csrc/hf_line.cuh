@@ -100,6 +100,12 @@ struct LineArgs {
   long long tile0, tile1;  // tile range of this launch (interior/boundary split of a slab)
   int reverse;             // walk the tile range backwards (alternating sweeps reuse L2, hf_tangent_set_alternate)
   long long cache_len;     // cache elements (bounds checks of the debug build)
+  // Hybrid tile schedule: the first `ks` rounds of the grid's warps are the
+  // static round robin; the remaining tiles are handed out one at a time from
+  // this counter (zero at launch; the last grab of the launch resets it).
+  // nullptr: static schedule only.
+  unsigned* dyn_ctr;
+  int ks;
 };
 
 // Per-warp line-buffer layout: element (cell m, component c, point i,j,k) at
@@ -548,15 +554,46 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   // the tile whose data a work slot processes: the range walked forwards, or
   // backwards when a.reverse (slots past the range stay past it)
   auto dtile = [&](long long tl) { return (a.reverse && tl < a.tile1) ? a.tile1 - 1 - (tl - a.tile0) : tl; };
-  // tile of this warp's k-th work item
-  // (round robin over blocks and warps; a global or per-SM dynamic schedule
-  // measured slower: DESIGN.md §4.1)
-  auto tile_k = [&](long long k) -> long long {
-    return dtile(a.tile0 + blockIdx.x + (warp + k * W) * (long long)gridDim.x);
+  // Tile schedule.  A warp's k-th work item is static for k < ks (round robin
+  // over blocks and warps: the tiles in flight at any time are one contiguous
+  // range) and then comes from a global counter, so that SMs that stream
+  // faster take more of the last tiles (the static schedule's warps exit
+  // between 34 and 49 us at config 2, tools/timeline.py).  A wholly dynamic
+  // schedule measured slower; only the tail is dynamic.  Every
+  // warp ends with exactly one failing grab, so the grab that returns
+  // dyn_tiles + warps - 1 is the launch's last and resets the counter.
+  const long long gw = blockIdx.x + warp * (long long)gridDim.x;
+  const long long wstride = (long long)W * gridDim.x;
+  const bool dyn = a.dyn_ctr != nullptr;
+  const long long dyn_base = a.tile0 + (long long)a.ks * wstride;
+  const unsigned dyn_tiles = dyn ? (unsigned)(a.tile1 - dyn_base) : 0u;
+  bool dyn_done = false;
+  unsigned pend = 0;       // lane 0: the raw counter value of the grab in flight
+  long long pend_t = 0;    // the static tile (or the end marker) of a request that needed no grab
+  bool pend_dyn = false;
+  auto request = [&](long long kk) {  // start obtaining work item kk
+    pend_dyn = false;
+    if (!dyn || kk < a.ks) {
+      pend_t = dtile(a.tile0 + gw + kk * wstride);
+    } else if (dyn_done) {
+      pend_t = a.tile1;
+    } else {
+      pend_dyn = true;
+      if (lane == 0) pend = atomicAdd(a.dyn_ctr, 1u);
+    }
   };
-  // chunk j of this warp: iq = j % N of its (j / N)-th tile
-  auto issue = [&](long long j) {
-    const long long tile = tile_k(j / N);
+  auto resolve = [&]() -> long long {  // the tile of the last request (>= ntiles: none)
+    if (!pend_dyn) return pend_t;
+    const unsigned v = __shfl_sync(0xffffffffu, pend, 0);
+    if (v >= dyn_tiles) {
+      dyn_done = true;
+      if (lane == 0 && v == dyn_tiles + (unsigned)wstride - 1u) atomicExch(a.dyn_ctr, 0u);
+      return a.tile1;
+    }
+    return dtile(dyn_base + (long long)v);
+  };
+  // chunk j of this warp (iq = j % N of tile `tile`, its (j / N)-th work item)
+  auto issue = [&](long long j, long long tile) {
     if (tile >= ntiles) return;
     const int s = (int)(j % RW);
     HF_ASSERT(tile * tstride + (j % N + 1) * CH <= a.cache_len);
@@ -577,13 +614,17 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   int slot, m, t;
   bool act;
   line_slot<DIM, N>(lane, slot, m, t, act);
+  request(0);
+  long long t_cur = resolve();  // this work item's tile and the next one's
+  request(1);
+  long long t_nxt = resolve();
   Gather<DIM, N, VAR> nxt;
-  gather_tile<DIM, N, VAR, ST>(a, tile_k(0), ntiles, m, t, act, nxt);
+  gather_tile<DIM, N, VAR, ST>(a, t_cur, ntiles, m, t, act, nxt);
   HF_TL(HF_TL_SLOTS - 4);
   if (lane == 0) {
     for (int s = 0; s < RW; ++s) mbar_init(full + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int j = 0; j < RW; ++j) issue(j);
+    for (int j = 0; j < RW; ++j) issue(j, t_cur);  // RW <= N: all of the first tile
   }
   __syncwarp();
   HF_TL(HF_TL_SLOTS - 3);
@@ -603,10 +644,11 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   long long jc = 0;  // this warp's chunk counter
   long long k = 0;
   for (;; ++k) {
-    if (tile_k(k) >= ntiles) break;
+    if (t_cur >= ntiles) break;
     HF_TL(1 + 4 * (int)k);
     const Gather<DIM, N, VAR> g = nxt;
-    gather_tile<DIM, N, VAR, ST>(a, tile_k(k + 1), ntiles, m, t, act, nxt);  // in flight during this tile
+    gather_tile<DIM, N, VAR, ST>(a, t_nxt, ntiles, m, t, act, nxt);  // in flight during this tile
+    request(k + 2);  // a grab has this whole tile to return
     const long long e = g.e;
     const bool live = g.live;
     double u[DIM][N];
@@ -749,7 +791,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       __syncwarp();
       if (lane < N) {  // stages consumed by every lane: lanes 0..N-1 refill them with the next tile's chunks
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(jc + lane + RW);
+        issue(jc + lane + RW, t_nxt);  // RW == N: the next tile's chunks
       }
       jc += N;
     } else {
@@ -764,7 +806,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
         __syncwarp();
         if (lane == 0) {  // stage consumed by every lane: refill it with chunk jc + RW
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(jc + RW);
+          issue(jc + RW, (jc + RW) / N == k ? t_cur : t_nxt);
         }
       }
     }
@@ -849,6 +891,8 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       }
     }
     __syncwarp();  // line buffers are reused by the next tile
+    t_cur = t_nxt;
+    t_nxt = resolve();
     HF_TL(4 + 4 * (int)k);
   }
   HF_TL(HF_TL_SLOTS - 1);
