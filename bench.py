@@ -547,6 +547,20 @@ def _extras(args, hbm, prob, ubar, x, y, flush, nqp):
     y3 = torch.empty_like(x3)
     nq3 = p3.mesh.n_elements * p3.n_qpoints_per_cell
     out["cfg3_q4"] = {s: variant(p3, wl3.ubar, x3, y3, s, nq3) for s in ("tensor4", "tensor2", "scalar")}
+    del x3, y3
+    # the same kernels on 8x the cells (6.44 M DoFs each): 64^3 Q2 (config 4's fine level) and
+    # 32^3 Q4.  At configs 2 and 3 a launch lasts 40-65 us, of which ~9 us are launch, first
+    # data and the drain of the last tiles; these sizes show the steady state.
+    if not args.no_newton:
+        for key, cid, mm in (("variants_64cubed_q2", 2, 64), ("variants_32cubed_q4", 3, 32)):
+            wlb = make_workload(cid, seed=0, m=mm)
+            pb = wlb.fine
+            xb = torch.from_numpy(wlb.x).cuda()
+            yb = torch.empty_like(xb)
+            nqb = pb.mesh.n_elements * pb.n_qpoints_per_cell
+            out[key] = {s: variant(pb, wlb.ubar, xb, yb, s, nqb) for s in ("tensor4", "tensor2", "scalar")}
+            out[key]["n_dofs"] = pb.n_dofs
+            del xb, yb, wlb, pb
     out["matrix_based"] = _matrix_based(prob, ubar, x, flush, hbm)
     out["cfg1"] = _cfg1(cpu=not args.no_cpu)
     if not args.no_newton:

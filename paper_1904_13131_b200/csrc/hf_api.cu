@@ -21,75 +21,6 @@
 
 using namespace hf;
 
-// ---- tile-queue counters of the apply kernel's hybrid schedule (hf_dispatch.h) ----
-// One zero-initialised block of counters per device.  Eager launches take the
-// counter of their stream (slots handed out from the front); launches being
-// captured into a graph take a fresh one each (from the back), never reused:
-// a graph may replay on any stream, concurrently with anything but itself.
-namespace hf {
-namespace {
-struct DynCounters {
-  static constexpr long long N = 1ll << 20;  // 4 MB
-  unsigned* base = nullptr;
-  long long front = 0, back = N;
-  std::map<cudaStream_t, unsigned*> by_stream;
-};
-std::mutex g_dyn_mu;
-std::map<int, DynCounters> g_dyn;
-int g_dyn_rounds = -2;
-}  // namespace
-
-int dyn_static_rounds(long long tiles, long long grid_warps) {
-  if (g_dyn_rounds == -2) {  // HF_DYN_ROUNDS: rounds left to the queue (0: static schedule)
-    const char* e = std::getenv("HF_DYN_ROUNDS");
-    g_dyn_rounds = e ? std::atoi(e) : 2;
-  }
-  if (g_dyn_rounds <= 0 || grid_warps <= 0) return -1;
-  const long long rounds = tiles / grid_warps;
-  // short launches keep the static schedule: every warp must reach the queue,
-  // and a queue over most of the range is the slow wholly dynamic schedule
-  if (rounds < g_dyn_rounds + 2) return -1;
-  return (int)(rounds - g_dyn_rounds);
-}
-
-// the device's counter block; allocated outside stream capture only
-static DynCounters* dyn_block(int dev, bool may_allocate) {
-  DynCounters& D = g_dyn[dev];
-  if (!D.base && may_allocate) {
-    unsigned* p = nullptr;
-    if (cudaMalloc((void**)&p, sizeof(unsigned) * DynCounters::N) != cudaSuccess ||
-        cudaMemset(p, 0, sizeof(unsigned) * DynCounters::N) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
-      cudaGetLastError();
-      if (p) cudaFree(p);
-      return nullptr;
-    }
-    D.base = p;
-  }
-  return D.base ? &D : nullptr;
-}
-
-unsigned* dyn_counter(cudaStream_t s) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(s, &st) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  std::lock_guard<std::mutex> lk(g_dyn_mu);
-  const bool capturing = st != cudaStreamCaptureStatusNone;
-  DynCounters* D = dyn_block(dev, !capturing);
-  if (!D) return nullptr;
-  if (capturing) return D->back - 1 > D->front ? D->base + --D->back : nullptr;
-  auto it = D->by_stream.find(s);
-  if (it != D->by_stream.end()) return it->second;
-  if (D->front + 1 >= D->back) return nullptr;
-  unsigned* c = D->base + D->front++;
-  D->by_stream.emplace(s, c);
-  return c;
-}
-}  // namespace hf
-
 namespace {
 thread_local std::string g_err;
 
@@ -254,7 +185,6 @@ struct hf_space {
   double* d_lam = nullptr;
   uint8_t* d_mask = nullptr;
   uint32_t* d_lmask = nullptr;  // per (cell, last-axis line): constraint bits (k_line_masks)
-  uint32_t* d_pmask = nullptr;  // 3D Q2: per (cell, z-plane) constraint bits (k_plane_masks)
   unsigned long long* d_u64 = nullptr;  // [0] detmin [1] detmax [2] first-index
 };
 
@@ -346,9 +276,6 @@ static cudaError_t update_cell_flags(hf_space* sp, cudaStream_t s) {
   if (sp->lat.n_el <= 0) return cudaSuccess;
   const long long n = sp->lat.n_el * (sp->dim == 3 ? sp->n1 * sp->n1 : sp->n1);
   k_line_masks<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(sp->lat, sp->dim, sp->degree, sp->d_mask, sp->d_lmask);
-  if (sp->d_pmask)
-    k_plane_masks<<<(unsigned)((sp->lat.n_el * 3 + 255) / 256), 256, 0, s>>>(sp->lat, sp->degree, sp->d_mask,
-                                                                            sp->d_pmask);
   return cudaGetLastError();
 }
 
@@ -498,7 +425,6 @@ HF_API int hf_space_create(int dim, int degree, int nq1, const int* cells, const
   ALLOC(sp->d_lam, sizeof(double) * nel);
   ALLOC(sp->d_mask, sp->n_dofs);
   ALLOC(sp->d_lmask, sizeof(uint32_t) * (nel > 0 ? nel : 1) * (dim == 3 ? N * N : N));
-  if (HF_PLANE_ENABLED && dim == 3 && N == 3) ALLOC(sp->d_pmask, sizeof(uint32_t) * (nel > 0 ? nel : 1) * 3);
   ALLOC(sp->d_u64, sizeof(unsigned long long) * 4);
   ALLOC(d_verts, sizeof(double) * nverts * dim);
   HF_CUDA(cudaMemcpyAsync(d_verts, vertices, sizeof(double) * nverts * dim, cudaMemcpyHostToDevice, s));
@@ -565,7 +491,6 @@ HF_API int hf_space_destroy(hf_space* sp) {
   dfree(sp->d_lam);
   dfree(sp->d_mask);
   dfree(sp->d_lmask);
-  dfree(sp->d_pmask);
   dfree(sp->d_u64);
   delete sp;
   return HF_OK;
@@ -585,7 +510,6 @@ static CellArgs base_args(const hf_space* sp) {
   a.lam = sp->d_lam;
   a.mask = sp->d_mask;
   a.lmask = sp->d_lmask;
-  a.pmask = sp->d_pmask;
   return a;
 }
 
@@ -663,7 +587,7 @@ HF_API int hf_tangent_create_ex(hf_space* sp, int strategy, int storage_bits, co
   op->nf = nfields(sp->dim, strategy);
   op->fp32 = storage_bits == 32;
   const int esz = op->fp32 ? 4 : 8;
-  const long long ncache = tile_cache_doubles(sp->dim, sp->n1, strategy, op->nf, sp->lat.n_el, esz);
+  const long long ncache = tile_cache_doubles(sp->dim, sp->n1, op->nf, sp->lat.n_el, esz);
   op->cache_len = ncache;
   HF_CUDA(dmalloc((void**)&op->d_cache, (size_t)esz * (ncache > 0 ? ncache : 1)));
   if (strategy == HF_SCALAR) {
@@ -773,7 +697,8 @@ HF_API int hf_tangent_apply_after_fill(hf_tangent* op, const double* x_dev, doub
 HF_API int hf_tangent_tiles(const hf_tangent* op, long long* n_tiles, int* cells_per_tile) {
   if (!op) return fail(HF_ERR_ARG, "null tangent");
   const hf_space* sp = op->sp;
-  const int cpw = tile_cells(sp->dim, sp->n1, op->strategy);
+  const int lines = sp->dim == 3 ? sp->n1 * sp->n1 : sp->n1;
+  const int cpw = 32 / lines;
   if (cells_per_tile) *cells_per_tile = cpw;
   if (n_tiles) *n_tiles = (sp->lat.n_el + cpw - 1) / cpw;
   return HF_OK;

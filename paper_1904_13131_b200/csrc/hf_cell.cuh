@@ -68,7 +68,6 @@ struct CellArgs {
   const double* ubar;       // scalar strategy: snapshot of the linearisation point
   const uint8_t* mask;      // [n_dofs] constrained DoFs
   const uint32_t* lmask;    // [n_el * lines] constraint bits per last-axis line (k_line_masks)
-  const uint32_t* pmask = nullptr;  // 3D Q2: [n_el * 3] constraint bits per (cell, z-plane) (k_plane_masks)
   const int* skip;          // optional device flag; non-zero -> kernel is a no-op
   int fill;                 // apply: 0 plain, 1/2 PDL secondary (hf_line.cuh LineArgs::fill)
   int fp32;                 // apply/build: cache and x/y stored as float (mixed-precision levels)
@@ -76,7 +75,6 @@ struct CellArgs {
   long long tile0, tile1;   // apply: tile range; tile1 < 0 means all tiles
   int reserve_sms = 0;      // apply: leave this many SMs' worth of blocks free (a concurrent NCCL kernel)
   int reverse = 0;          // apply: walk the tile range backwards
-  int no_dyn = 0;           // apply: static tile schedule only
   unsigned long long* detmin;  // ordered-double min of det F (build / residual / range)
   unsigned long long* detmax;
 };
@@ -446,7 +444,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_build(const CellArgs a) {
   warp_minmax_atomic(a.detmin, nullptr, t.act ? k.J : 0.0, t.act);
   if (!t.act) return;
   constexpr int NF = CacheFields<DIM, VAR>::NF;
-  using TL = CacheLayout<DIM, N, VAR>;
+  using TL = TileLayout<DIM, N>;
   ST* o = reinterpret_cast<ST*>(a.cache_out);  // fp64, or fp32 storage of a mixed-precision level
   auto put = [&](int f, double v) {
     const long long i = TL::template index_e<sizeof(ST)>(t.e, t.lq, f, NF);
@@ -525,7 +523,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_diag(const CellArgs a) {
       const double mu = __ldg(a.mu + t.e), lam = __ldg(a.lam + t.e);
       Kin<DIM> k;
       kinematics<DIM>(gub, ji, mu, lam, k, true);
-      const double c1 = a.cache[CacheLayout<DIM, N, VAR>::index(t.e, t.lq, 0, NF)];  // cached c1 (same value as k.c1)
+      const double c1 = a.cache[TileLayout<DIM, N>::index(t.e, t.lq, 0, NF)];  // cached c1 (same value as k.c1)
 #pragma unroll
       for (int i = 0; i < DIM; ++i)
 #pragma unroll
@@ -546,7 +544,7 @@ __global__ void __launch_bounds__(Cfg<DIM, N>::NT) k_diag(const CellArgs a) {
   } else if (t.act) {
     double cf[NF];
 #pragma unroll
-    for (int f = 0; f < NF; ++f) cf[f] = a.cache[CacheLayout<DIM, N, VAR>::index(t.e, t.lq, f, NF)];
+    for (int f = 0; f < NF; ++f) cf[f] = a.cache[TileLayout<DIM, N>::index(t.e, t.lq, f, NF)];
     const int off = (VAR == TENSOR2) ? 2 : 0;
 #pragma unroll
     for (int i = 0; i < DIM; ++i)
@@ -862,32 +860,6 @@ static __global__ void k_line_masks(const HfLattice lat, int dim, int degree, co
                                     : (long long)(ex * degree + i) + (long long)lat.nodes[0] * (long long)(ey * degree + l);
     for (int c = 0; c < dim; ++c)
       if (mask[node * dim + c]) b |= 1u << (c * n1 + l);
-  }
-  bits[id] = b;
-}
-
-
-// Constraint bits of every (cell, z-plane) of a 3D Q2 lattice for the plane
-// kernel (hf_plane.cuh): bit c*9 + a + 3b is set when DoF c of node (a, b) of
-// plane k is constrained.
-static __global__ void k_plane_masks(const HfLattice lat, int degree, const uint8_t* __restrict__ mask,
-                                     uint32_t* __restrict__ bits) {
-  const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= lat.n_el * 3) return;
-  const long long e = id / 3;
-  const int k = (int)(id - e * 3);
-  long long r = e;
-  const int ex = (int)(r % lat.cells[0]);
-  r /= lat.cells[0];
-  const int ey = (int)(r % lat.cells[1]);
-  const int ez = (int)(r / lat.cells[1]);
-  uint32_t b = 0;
-  for (int q = 0; q < 9; ++q) {
-    const long long node = (long long)(ex * degree + q % 3) +
-                           (long long)lat.nodes[0] * ((long long)(ey * degree + q / 3) +
-                                                      (long long)lat.nodes[1] * (long long)(ez * degree + k));
-    for (int c = 0; c < 3; ++c)
-      if (mask[node * 3 + c]) b |= 1u << (c * 9 + q);
   }
   bits[id] = b;
 }

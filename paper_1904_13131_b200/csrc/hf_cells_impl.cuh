@@ -2,7 +2,6 @@
 #pragma once
 #include "hf_dispatch.h"
 #include "hf_line.cuh"
-#include "hf_plane.cuh"
 
 
 namespace hf {
@@ -76,11 +75,6 @@ cudaError_t launch_apply_line_t(const CellArgs& c, cudaStream_t s) {
   if (c.reserve_sms > 0 && cap > 2ll * c.reserve_sms) cap -= (cap / (nsm_cached() > 0 ? nsm_cached() : 148)) * c.reserve_sms;
   if (nb > cap) nb = cap;
   if (nb <= 0) return cudaSuccess;
-  // hybrid schedule: the last rounds' tiles come from a queue (hf_line.cuh)
-  a.dyn_ctr = nullptr;
-  a.ks = 0;
-  const int ks = c.no_dyn ? -1 : dyn_static_rounds(tiles, nb * PL::W);
-  if (ks >= 0 && (a.dyn_ctr = dyn_counter(s)) != nullptr) a.ks = ks;
   if (!c.fill) {
     kern<<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T);
     return cudaGetLastError();
@@ -99,70 +93,8 @@ cudaError_t launch_apply_line_t(const CellArgs& c, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, a, T);
 }
 
-// Launch of the plane-parallel apply (hf_plane.cuh; 3D Q2, tensor2 cache).
-template <int VAR, typename ST>
-cudaError_t launch_apply_plane_t(const CellArgs& c, cudaStream_t s) {
-  using PL = PlanePlan<VAR, ST>;
-  constexpr auto kern = k_apply_plane<VAR, ST>;
-  static int resident = -1;
-  if (resident < 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::SMEM);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PL::NT, PL::SMEM);
-    if (e != cudaSuccess) return e;
-    resident = (per_sm > 0 ? per_sm : 1) * (nsm_cached() > 0 ? nsm_cached() : 148);
-  }
-  if (!c.pmask) return cudaErrorInvalidValue;
-  LineArgs a = {};
-  a.lat = c.lat;
-  a.degree = c.degree;
-  a.x = c.x;
-  a.y = c.y;
-  a.cache = c.cache;
-  a.mask = c.mask;
-  a.skip = c.skip;
-  a.fill = c.fill;
-  a.cache_len = c.cache_len;
-  a.reverse = c.reverse;
-  const long long all_tiles = (c.lat.n_el + PlaneCfg::CPW - 1) / PlaneCfg::CPW;
-  a.tile0 = c.tile1 < 0 ? 0 : c.tile0;
-  a.tile1 = c.tile1 < 0 ? all_tiles : (c.tile1 < all_tiles ? c.tile1 : all_tiles);
-  TabPlane T = {};
-  for (int l = 0; l < 3; ++l)
-    for (int o = 0; o < 3; ++o) {
-      T.V[l][o] = c.tab.V[l * 3 + o];
-      T.D[l][o] = c.tab.D[l * 3 + o];
-      T.Dc[l][o] = c.tab.Dc[l * 3 + o];
-    }
-  const long long tiles = a.tile1 - a.tile0;
-  long long nb = tiles;
-  long long cap = resident;
-  if (c.reserve_sms > 0 && cap > 2ll * c.reserve_sms) cap -= (cap / (nsm_cached() > 0 ? nsm_cached() : 148)) * c.reserve_sms;
-  if (nb > cap) nb = cap;
-  if (nb <= 0) return cudaSuccess;
-  if (!c.fill) {
-    kern<<<(unsigned)nb, PL::NT, PL::SMEM, s>>>(a, T, c.pmask);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)nb);
-  cfg.blockDim = dim3(PL::NT);
-  cfg.dynamicSmemBytes = PL::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, T, c.pmask);
-}
-
 template <int DIM, int N, int VAR>
 cudaError_t launch_apply_line(const CellArgs& c, cudaStream_t s) {
-  if constexpr (CacheLayout<DIM, N, VAR>::PLANE)
-    return c.fp32 ? launch_apply_plane_t<VAR, float>(c, s) : launch_apply_plane_t<VAR, double>(c, s);
-  else
   return c.fp32 ? launch_apply_line_t<DIM, N, VAR, float>(c, s) : launch_apply_line_t<DIM, N, VAR, double>(c, s);
 }
 

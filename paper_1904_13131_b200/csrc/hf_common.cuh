@@ -180,53 +180,12 @@ struct TileLayout {
     return tile * (N * chunk_e<ESZ>(nf)) + iq * chunk_e<ESZ>(nf) + (long long)f * K::LANES + m * K::L + line;
   }
 };
-// The plane-parallel apply kernel (hf_plane.cuh) serves 3D Q2 with the tensor2
-// cache (variant 1) unless the library is built with -DHF_NO_PLANE (A/B builds).
-#ifdef HF_NO_PLANE
-#define HF_PLANE_ENABLED 0
-#else
-#define HF_PLANE_ENABLED 1
-#endif
-
-// Cache layout of one (DIM, N, caching variant): the line kernel's tiles
-// (TileLayout), or for the plane kernel [tile of 10 cells][p][field][lane]
-// with p = the point within a z-plane (x fastest) and lane = cell * 3 + plane.
-template <int DIM, int N, int VAR>
-struct CacheLayout {
-  static constexpr bool PLANE = HF_PLANE_ENABLED && DIM == 3 && N == 3 && VAR == 1;
-  using K = LineCfg<DIM, N>;
-  static constexpr int CPW = PLANE ? 10 : K::CPW;        // cells per warp tile
-  static constexpr int LANES = PLANE ? 30 : K::LANES;    // active lanes
-  static constexpr int CHUNKS = PLANE ? 9 : N;           // TMA chunks per tile
-  template <int ESZ = 8>
-  HF_DEV static constexpr long long chunk_e(int nf) {
-    return ((long long)nf * LANES + (16 / ESZ - 1)) & ~(long long)(16 / ESZ - 1);
-  }
-  // flat index of field f of (cell e, local q-point lq, x fastest) for ESZ-byte elements
-  template <int ESZ = 8>
-  HF_DEV static long long index_e(long long e, int lq, int f, int nf) {
-    const long long tile = e / CPW;
-    const int m = (int)(e - tile * CPW);
-    const int c = PLANE ? lq % 9 : lq % N;
-    const int ln = PLANE ? m * 3 + lq / 9 : m * K::L + lq / N;
-    return (tile * CHUNKS + c) * chunk_e<ESZ>(nf) + (long long)f * LANES + ln;
-  }
-  HF_DEV static long long index(long long e, int lq, int f, int nf) { return index_e<8>(e, lq, f, nf); }
-};
-
-// cells per tile / elements of esz bytes of the tiled cache (host side)
-inline int tile_cells(int dim, int n1, int var) {
-  if (HF_PLANE_ENABLED && dim == 3 && n1 == 3 && var == 1) return 10;
-  return 32 / (dim == 3 ? n1 * n1 : n1);
-}
-inline long long tile_cache_doubles(int dim, int n1, int var, int nf, long long n_el, int esz = 8) {
-  const bool plane = HF_PLANE_ENABLED && dim == 3 && n1 == 3 && var == 1;
-  const int lines = dim == 3 ? n1 * n1 : n1;
-  const int cpw = tile_cells(dim, n1, var);
-  const int lanes = plane ? 30 : cpw * lines;
-  const int chunks = plane ? 9 : n1;
+inline long long tile_cache_doubles(int dim, int n1, int nf, long long n_el, int esz = 8) {
+  int nq = dim == 2 ? n1 * n1 : n1 * n1 * n1;
+  int lanes = (32 / (nq / n1)) * (nq / n1);
+  int cpw = 32 / (nq / n1);
   long long tiles = (n_el + cpw - 1) / cpw;
   const long long r = 16 / esz - 1;
   long long ch = ((long long)nf * lanes + r) & ~r;
-  return tiles * chunks * ch;  // elements of esz bytes
+  return tiles * n1 * ch;  // elements of esz bytes
 }

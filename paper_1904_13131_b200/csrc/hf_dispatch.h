@@ -25,15 +25,6 @@ cudaError_t launch_cell_dofs(const HfLattice& lat, int dim, int degree, long lon
 #define HF_TL_SLOTS 72
 cudaError_t timeline_copy_3d(unsigned long long* host, int clear);
 
-// Tile-queue counter of one apply launch on stream s (hf_line.cuh, the hybrid
-// schedule): zero when the launch starts and again when it ends.  Launches on
-// one stream run one after the other and share a counter; a launch recorded
-// into a CUDA graph gets a counter of its own (graphs replay on any stream).
-// nullptr (static schedule) when no counter is available.
-unsigned* dyn_counter(cudaStream_t s);
-// static rounds before the queue takes over, or -1: static schedule only
-int dyn_static_rounds(long long tiles, long long grid_warps);
-
 // blocks per grid and cells per block of the cell kernels
 int cells_per_block(int dim, int n1);
 

@@ -100,12 +100,6 @@ struct LineArgs {
   long long tile0, tile1;  // tile range of this launch (interior/boundary split of a slab)
   int reverse;             // walk the tile range backwards (alternating sweeps reuse L2, hf_tangent_set_alternate)
   long long cache_len;     // cache elements (bounds checks of the debug build)
-  // Hybrid tile schedule: the first `ks` rounds of the grid's warps are the
-  // static round robin; the remaining tiles are handed out one at a time from
-  // this counter (zero at launch; the last grab of the launch resets it).
-  // nullptr: static schedule only.
-  unsigned* dyn_ctr;
-  int ks;
 };
 
 // Per-warp line-buffer layout: element (cell m, component c, point i,j,k) at
@@ -554,51 +548,24 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   // the tile whose data a work slot processes: the range walked forwards, or
   // backwards when a.reverse (slots past the range stay past it)
   auto dtile = [&](long long tl) { return (a.reverse && tl < a.tile1) ? a.tile1 - 1 - (tl - a.tile0) : tl; };
-  // Tile schedule.  A warp's k-th work item is static for k < ks (round robin
-  // over blocks and warps: the tiles in flight at any time are one contiguous
-  // range) and then comes from a global counter, so that SMs that stream
-  // faster take more of the last tiles (the static schedule's warps exit
-  // between 34 and 49 us at config 2, tools/timeline.py).  A wholly dynamic
-  // schedule measured slower; only the tail is dynamic.  Every
-  // warp ends with exactly one failing grab, so the grab that returns
-  // dyn_tiles + warps - 1 is the launch's last and resets the counter.
-  const long long gw = blockIdx.x + warp * (long long)gridDim.x;
-  const long long wstride = (long long)W * gridDim.x;
-  const bool dyn = a.dyn_ctr != nullptr;
-  const long long dyn_base = a.tile0 + (long long)a.ks * wstride;
-  const unsigned dyn_tiles = dyn ? (unsigned)(a.tile1 - dyn_base) : 0u;
-  bool dyn_done = false;
-  unsigned pend = 0;       // lane 0: the raw counter value of the grab in flight
-  long long pend_t = 0;    // the static tile (or the end marker) of a request that needed no grab
-  bool pend_dyn = false;
-  auto request = [&](long long kk) {  // start obtaining work item kk
-    pend_dyn = false;
-    if (!dyn || kk < a.ks) {
-      pend_t = dtile(a.tile0 + gw + kk * wstride);
-    } else if (dyn_done) {
-      pend_t = a.tile1;
-    } else {
-      pend_dyn = true;
-      if (lane == 0) pend = atomicAdd(a.dyn_ctr, 1u);
-    }
+  // tile of this warp's k-th work item
+  // (round robin over blocks and warps; a global or per-SM dynamic schedule
+  // measured slower: DESIGN.md §4.1)
+  auto tile_k = [&](int k) -> long long {
+    return dtile(a.tile0 + blockIdx.x + (warp + (long long)k * W) * (long long)gridDim.x);
   };
-  auto resolve = [&]() -> long long {  // the tile of the last request (>= ntiles: none)
-    if (!pend_dyn) return pend_t;
-    const unsigned v = __shfl_sync(0xffffffffu, pend, 0);
-    if (v >= dyn_tiles) {
-      dyn_done = true;
-      if (lane == 0 && v == dyn_tiles + (unsigned)wstride - 1u) atomicExch(a.dyn_ctr, 0u);
-      return a.tile1;
-    }
-    return dtile(dyn_base + (long long)v);
+  // a tile's cache block (nullptr past the range): formed once per tile, so
+  // that issuing a chunk is a multiply-free handful of instructions (the
+  // per-chunk 64-bit tile arithmetic was 12 % of the Q4 kernel's instructions)
+  auto cblock = [&](long long tile) -> const ST* {
+    HF_ASSERT(tile >= ntiles || (tile + 1) * tstride <= a.cache_len);
+    return tile < ntiles ? cache + tile * tstride : nullptr;
   };
-  // chunk j of this warp (iq = j % N of tile `tile`, its (j / N)-th work item)
-  auto issue = [&](long long j, long long tile) {
-    if (tile >= ntiles) return;
-    const int s = (int)(j % RW);
-    HF_ASSERT(tile * tstride + (j % N + 1) * CH <= a.cache_len);
+  // chunk c (iq) of the cache block cb into ring stage s
+  auto issue = [&](const ST* cb, int c, int s) {
+    if (!cb) return;
     mbar_expect_tx(full + s, (unsigned)(CH * sizeof(ST)));
-    tma_load_1d(ring + (size_t)s * CH, cache + tile * tstride + (j % N) * CH, (unsigned)(CH * sizeof(ST)), full + s);
+    tma_load_1d(ring + (size_t)s * CH, cb + (size_t)c * CH, (unsigned)(CH * sizeof(ST)), full + s);
   };
   // y = mask ? x : 0 is written by the preceding k_fill_masked launch.  With
   // programmatic dependent launch (a.fill != 0) this kernel starts while that
@@ -614,17 +581,15 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   int slot, m, t;
   bool act;
   line_slot<DIM, N>(lane, slot, m, t, act);
-  request(0);
-  long long t_cur = resolve();  // this work item's tile and the next one's
-  request(1);
-  long long t_nxt = resolve();
   Gather<DIM, N, VAR> nxt;
+  long long t_cur = tile_k(0);  // this work item's tile and the next one's
   gather_tile<DIM, N, VAR, ST>(a, t_cur, ntiles, m, t, act, nxt);
   HF_TL(HF_TL_SLOTS - 4);
+  const ST* cb_cur = cblock(t_cur);
   if (lane == 0) {
     for (int s = 0; s < RW; ++s) mbar_init(full + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int j = 0; j < RW; ++j) issue(j, t_cur);  // RW <= N: all of the first tile
+    for (int j = 0; j < RW; ++j) issue(cb_cur, j, j);  // RW <= N: chunks of the first tile
   }
   __syncwarp();
   HF_TL(HF_TL_SLOTS - 3);
@@ -641,14 +606,15 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   double* A = bufs[0];  // values at the Gauss points -> G1 (in place) -> queued y part -> result
   double* B = bufs[1];  // scratch -> G2 -> queued z part
 
-  long long jc = 0;  // this warp's chunk counter
-  long long k = 0;
+  unsigned jc = 0;  // this warp's chunk counter
+  int k = 0;
   for (;; ++k) {
     if (t_cur >= ntiles) break;
     HF_TL(1 + 4 * (int)k);
+    const long long t_nxt = tile_k(k + 1);
+    const ST* cb_nxt = cblock(t_nxt);
     const Gather<DIM, N, VAR> g = nxt;
     gather_tile<DIM, N, VAR, ST>(a, t_nxt, ntiles, m, t, act, nxt);  // in flight during this tile
-    request(k + 2);  // a grab has this whole tile to return
     const long long e = g.e;
     const bool live = g.live;
     double u[DIM][N];
@@ -782,16 +748,17 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     }
     };
     if constexpr (RW >= N) {
+      static_assert(RW <= N, "a ring at least a tile deep is exactly a tile deep");
       // the whole tile's chunks are resident: wait once, then the N points
       // are free of barriers and the compiler interleaves their chains
 #pragma unroll
-      for (int iq = 0; iq < N; ++iq) mbar_wait(full + (int)((jc + iq) % RW), (unsigned)(((jc + iq) / RW) & 1));
+      for (int iq = 0; iq < N; ++iq) mbar_wait(full + iq, (unsigned)k & 1u);  // RW == N: chunk iq sits in stage iq
 #pragma unroll
-      for (int iq = 0; iq < N; ++iq) point(iq, ring + (size_t)((jc + iq) % RW) * CH + slot);
+      for (int iq = 0; iq < N; ++iq) point(iq, ring + (size_t)iq * CH + slot);
       __syncwarp();
       if (lane < N) {  // stages consumed by every lane: lanes 0..N-1 refill them with the next tile's chunks
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(jc + lane + RW, t_nxt);  // RW == N: the next tile's chunks
+        issue(cb_nxt, lane, lane);  // RW == N: the next tile's chunks
       }
       jc += N;
     } else {
@@ -801,12 +768,15 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
 #pragma unroll(ROLL ? 1 : N)
       for (int iq = 0; iq < N; ++iq, ++jc) {
         const int s = (int)(jc % RW);
-        mbar_wait(full + s, (unsigned)((jc / RW) & 1));
+        mbar_wait(full + s, (jc / RW) & 1u);
         point(iq, ring + (size_t)s * CH + slot);
         __syncwarp();
         if (lane == 0) {  // stage consumed by every lane: refill it with chunk jc + RW
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(jc + RW, (jc + RW) / N == k ? t_cur : t_nxt);
+          if (iq + RW < N)
+            issue(cb_cur, iq + RW, s);
+          else
+            issue(cb_nxt, iq + RW - N, s);
         }
       }
     }
@@ -892,7 +862,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     }
     __syncwarp();  // line buffers are reused by the next tile
     t_cur = t_nxt;
-    t_nxt = resolve();
+    cb_cur = cb_nxt;
     HF_TL(4 + 4 * (int)k);
   }
   HF_TL(HF_TL_SLOTS - 1);
