@@ -379,10 +379,14 @@ def _init_dist(ws, local):
     backend = os.environ.get("HF_BENCH_BACKEND", "nccl")
     dev = local % torch.cuda.device_count()
     torch.cuda.set_device(dev)
+    # a rank that fails alone must not leave the others in a collective for NCCL's default 10 minutes
+    from datetime import timedelta
+
+    tmo = timedelta(seconds=int(os.environ.get("HF_BENCH_DIST_TIMEOUT_S", "300")))
     if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev), timeout=tmo)
     else:
-        dist.init_process_group(backend)
+        dist.init_process_group(backend, timeout=tmo)
 
 
 def _headline_single(args, flush):
@@ -476,9 +480,15 @@ def run_ours(args):
         if ws == 1:
             line["cfg5_strong"] = _cfg5(LocalComm(), 10, 3)
         else:
-            line["cfg2_weak"] = _cfg2_weak(args, TorchComm(), flush)
-            if not args.no_newton:
-                line["newton_slabs"] = _dist_newton(TorchComm())
+            # extras after the headline: an exception here (raised on every rank alike) is recorded, not fatal
+            for key, fn in (("cfg2_weak", lambda: _cfg2_weak(args, TorchComm(), flush)),
+                            ("newton_slabs", (lambda: _dist_newton(TorchComm())) if not args.no_newton else None)):
+                if fn is None:
+                    continue
+                try:
+                    line[key] = fn()
+                except Exception as exc:  # noqa: BLE001
+                    line[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     if rank == 0 and ws == 1 and not args.no_cpu:
         from oracle import ref
 

@@ -46,6 +46,7 @@ def refside():
     sys.modules["hyperfree._b200"] = mod
     exec(compile(stub_source(), mod.__file__, "exec"), mod.__dict__)
     saved = (hf.operators.MatrixFreeTangent, hf.multigrid.MatrixFreeTangent)
+    mod.reference_operator = saved[0]  # the reference's own class, for side-by-side checks
     mod.install()
     yield hf, mod
     hf.operators.MatrixFreeTangent, hf.multigrid.MatrixFreeTangent = saved
@@ -103,3 +104,43 @@ def test_reference_nonpositive_jacobian_through_stub(refside):
     with pytest.raises(hf.material.NonPositiveJacobian) as ei:
         hf.operators.make_tangent(prob, g["bad_state"], "tensor4")
     assert ei.value.element == int(g["bad_element"])
+
+
+# the reference's own self-checks (verify.py) that construct MatrixFreeTangent:
+# strategies vs the reference's assembled matrix (verify.py:70-84), the tangent
+# vs central differences of the reference's residual (87-104), the diagonal vs
+# the assembled one (158-165), the cache payload counts (168-178)
+VERIFY_CHECKS = ["check_strategy_equivalence", "check_tangent_fd", "check_diagonal", "check_payload_counts"]
+
+
+@pytest.mark.parametrize("check", VERIFY_CHECKS)
+def test_reference_verify_checks_on_libhf(refside, check, monkeypatch):
+    """``hyperfree verify`` (verify.py:199-217) with the B200 operator bound:
+    the reference's own thresholds, its own AssembledTangent / compute_residual
+    on the CPU as the independent side."""
+    hf, mod = refside
+    import importlib
+
+    verify = importlib.import_module("hyperfree.verify")
+    built = []
+
+    class Counting(mod.MatrixFreeTangent):
+        def __init__(self, *a, **k):
+            super().__init__(*a, **k)
+            built.append(self.strategy)
+
+    monkeypatch.setattr(verify, "MatrixFreeTangent", mod.reference_operator)
+    want = getattr(verify, check)(0)  # the unmodified reference, on the CPU
+    monkeypatch.setattr(verify, "MatrixFreeTangent", Counting)
+    rec = getattr(verify, check)(0)
+    assert built, "the check did not construct the B200 operator"
+    # same verdict as the reference's own operator, and the same measured value
+    # where the value is a convergence order (the reference's finite-difference
+    # slope check fails its own 1.8 threshold at this seed: 1.69, SURVEY 8(c)
+    # calls it fragile; the B200 operator must reproduce that number)
+    assert bool(rec.passed) == bool(want.passed), (rec, want)
+    if check == "check_tangent_fd":
+        assert rec.value == pytest.approx(want.value, rel=1e-5), (rec, want)
+    else:
+        assert rec.passed, f"{rec.name}: {rec.value} against the reference's threshold {rec.threshold}"
+
