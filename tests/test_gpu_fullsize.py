@@ -341,3 +341,42 @@ def test_tile_range_apply_with_reserved_sms():
         op.apply_tiles(x, y, 0, cut, reserve_sms=reserve)
         op.apply_tiles(x, y, cut, nt, reserve_sms=reserve)
         assert _rel(y, ref) < 1e-14
+
+
+@pytest.mark.parametrize("dim,degree,m", [(2, 5, 6), (2, 6, 5), (2, 7, 5), (2, 8, 4), (3, 1, 7), (3, 3, 5)])
+def test_every_instantiated_degree_vs_oracle_and_reference(dim, degree, m):
+    """The degrees the golden files do not hold (2D Q5-Q8: warp tiles of 5, 4, 4
+    and 3 cells; 3D Q1 and Q3 on a mesh whose cell count is not a multiple of the
+    tile): apply of every caching variant, diagonal and residual against the
+    oracle, and apply / residual against the unmodified reference itself."""
+    from oracle import ref
+    from paper_1904_13131_b200 import MatrixFreeTangent, Problem, build_benchmark_mesh, compute_residual
+    from paper_1904_13131_b200.workloads import MATERIAL, clamp_weighted_sine, constrain
+
+    rng = np.random.default_rng(degree * 10 + dim)
+    centres = rng.random((3, dim))
+    radius = 0.2
+    p = Problem(build_benchmark_mesh(dim, m, [(c, radius) for c in centres], side=1.0), degree, MATERIAL)
+    constrain(p, 0)
+    ubar = clamp_weighted_sine(dim, m, degree, 2.0 * np.pi * rng.random((dim, dim)), 0.03, 0)
+    x = rng.standard_normal(p.n_dofs)
+    op_ = _oracle_of(p)
+    for s in O.STRATEGIES:
+        op = MatrixFreeTangent(p, ubar, s)
+        y = op.apply(x)
+        yo = O.Tangent(op_, ubar, s).apply(x)
+        assert np.linalg.norm(y - yo) / np.linalg.norm(yo) < TOL, s
+        d = np.asarray(op.diagonal())
+        do = O.Tangent(op_, ubar, s).diagonal()
+        assert np.linalg.norm(d - do) / np.linalg.norm(do) < TOL, s
+    traction = np.array([0.01, -0.02, 0.03])[:dim]
+    r = compute_residual(p, ubar, traction)
+    ro = O.residual(op_, ubar, traction)
+    assert np.linalg.norm(r - ro) / np.linalg.norm(ro) < TOL
+    if ref.available():
+        hf = ref.hyperfree()
+        rp = ref.problem(hf, dim, m, degree, centres, radius, p.constraints.mask)
+        yr = hf.operators.MatrixFreeTangent(rp, ubar, "tensor4").apply(x)
+        assert np.linalg.norm(MatrixFreeTangent(p, ubar, "tensor4").apply(x) - yr) / np.linalg.norm(yr) < TOL
+        rr = hf.operators.compute_residual(rp, ubar, traction)
+        assert np.linalg.norm(r - rr) / np.linalg.norm(rr) < TOL

@@ -12,3 +12,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:k_apply_line --launch-skip 2 --launch-count 1 \
     -f -o gpurun_out/final2/ncu_tensor4_2 python tools/prof_variant.py tensor4 2 4 > gpurun_out/final2/ncu_tensor4_2.log 2>&1; echo "ncu rc=$?"
 tail -n 3 gpurun_out/final2/pytest_gpu.log gpurun_out/final2/smoke.log
+for v in "tensor2 2" "scalar 2" "tensor4 3" "tensor2 3" "scalar 3"; do
+  set -- $v
+  timeout 300 ncu --set full --import-source on --clock-control none -k regex:k_apply_line --launch-skip 2 --launch-count 1 \
+    -f -o gpurun_out/final2/ncu_$1_$2 python tools/prof_variant.py $1 $2 4 > gpurun_out/final2/ncu_$1_$2.log 2>&1; echo "ncu $v rc=$?"
+done
+HF_BENCH_BACKEND=gloo timeout 600 python bench.py --gpus 2 --steps 5 --warmup 3 --no-newton > gpurun_out/final2/bench_n2_gloo.json 2> gpurun_out/final2/bench_n2_gloo.err; echo "n2 rc=$?"
