@@ -497,10 +497,16 @@ def run_ours(args):
                                 "sample": f"{what}: {n} applies after 1 warm-up ({dt:.2f} s each), 1 BLAS thread "
                                           "(the numpy path is single-core: SURVEY P2)",
                                 "cpu_model": ref.cpu_model(), "host_cpus": os.cpu_count()}
+    if ws > 1:
+        # NCCL's INFO lines go to stdout: tear the group down first and let the other ranks' last
+        # lines drain, so that the JSON line is the last line of the run
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+        if rank == 0:
+            sys.stdout.flush()
+            time.sleep(1.0)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.destroy_process_group()
 
 
 def _cfg2_weak(args, comm, flush):
