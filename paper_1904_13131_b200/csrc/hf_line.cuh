@@ -537,6 +537,14 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   constexpr int NM = NV * (NV + 1) / 2;
   if (a.skip && *a.skip) return;
   HF_TL(0);
+#ifdef HF_TIMELINE
+  {  // the SM this block runs on (slot SLOTS - 5), for per-SM speed statistics
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const unsigned w_ = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if ((threadIdx.x & 31) == 0 && w_ < HF_TL_WARPS) hf_tl_buf[w_ * HF_TL_SLOTS + HF_TL_SLOTS - 5] = smid + 1;
+  }
+#endif
   extern __shared__ __align__(128) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ST* ring = reinterpret_cast<ST*>(smem) + (size_t)warp * RW * CH;  // this warp's stages (16-byte aligned)

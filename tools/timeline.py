@@ -38,9 +38,12 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
 check(lib().hf_timeline_fetch(buf.ctypes.data, buf.size, 1))
-t = buf.reshape(WARPS, SLOTS).astype(np.float64)
+raw = buf.reshape(WARPS, SLOTS)
+t = raw.astype(np.float64)
 used = t[:, 0] > 0
+smid = raw[used, SLOTS - 5].astype(np.int64) - 1  # the SM of each warp's block (-1: not recorded)
 t = t[used]
+t[:, SLOTS - 5] = 0
 t0 = t[:, 0].min()
 t = np.where(t > 0, t - t0, np.nan)
 entry, exit_ = t[:, 0], t[:, SLOTS - 1]
@@ -73,3 +76,5 @@ res = {"strategy": s, "cfg": cfg, "event_ms": ms, "warps": int(used.sum()),
 print(json.dumps(res))
 np.save(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out",
                      f"timeline_{s}_{cfg}.npy"), t)
+np.save(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out",
+                     f"timeline_{s}_{cfg}_smid.npy"), smid)
