@@ -33,6 +33,7 @@ cores, with the same ``config``.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -895,8 +896,10 @@ def _newton_solve_cfg4(strategy="tensor4"):
 def _newton_iteration(coarse_precision="fp64"):
     """First Newton iteration of load step 1 of config 4 (64^3 Q2, levels 4..64,
     prescribed top displacement): tangent + GMG build, CG to 1e-6
-    (NewtonSettings.linear_rel_tol, solver.py:85), residual.  Run twice; the
-    second (warm) run is reported.  coarse_precision="fp32": every GMG level
+    (NewtonSettings.linear_rel_tol, solver.py:85), residual.  Run four times;
+    the fastest of the three warm runs is reported and all three are listed
+    (``runs_s``: a one-off 0.1 s stall lands in one run of some bench
+    processes).  coarse_precision="fp32": every GMG level
     below the finest in fp32 storage."""
     import torch
 
@@ -909,11 +912,14 @@ def _newton_iteration(coarse_precision="fp64"):
     fine = probs[-1]
     X = node_coordinates(fine.mesh, fine.dofmap)
     transfers = build_transfers(probs)
-    rec = None
-    for _ in range(2):
+    rec, runs = None, []
+    for run in range(4):
         u = torch.zeros(fine.n_dofs, dtype=torch.float64, device="cuda")
         u.view(-1, 3)[:, 2] += (-0.05 / 5) * torch.from_numpy(X[:, 2] / X[:, 2].max()).cuda()
         res = compute_residual(fine, u)
+        # handles of earlier sections that are still cyclic garbage would be destroyed (a device
+        # synchronisation each) whenever the collector next runs, e.g. in the middle of the timed CG
+        gc.collect()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         op = MatrixFreeTangent(fine, u, "tensor4")
@@ -928,11 +934,18 @@ def _newton_iteration(coarse_precision="fp64"):
         res = compute_residual(fine, u)
         torch.cuda.synchronize()
         t3 = time.perf_counter()
-        rec = {"workload": "cfg4 64^3 Q2 levels 4..64, load step 1, Newton iteration 1", "n_dofs": fine.n_dofs,
+        cur = {"workload": "cfg4 64^3 Q2 levels 4..64, load step 1, Newton iteration 1", "n_dofs": fine.n_dofs,
                "coarse_levels": coarse_precision,
                "newton_iteration_s": t3 - t0, "setup_s": t1 - t0, "cg_s": t2 - t1, "cg_iterations": rep.iterations,
                "s_per_cg_iteration": (t2 - t1) / max(rep.iterations, 1)}
         del op, gmg
+        if run == 0:
+            continue  # cold: allocations, first graph capture
+        runs.append(cur["newton_iteration_s"])
+        if rec is None or cur["newton_iteration_s"] < rec["newton_iteration_s"]:
+            rec = cur
+    rec["runs_s"] = runs
+    rec["stat"] = "fastest of 3 warm runs (each: tangent + GMG build, CG with its V-cycle graph capture, residual)"
     return rec
 
 
