@@ -178,6 +178,18 @@ HF_API int hf_tangent_host_info(const hf_tangent* op, int* variant, float* us4);
 /* diagnostic: per-warp timestamps of the last apply of an instrumented build
  * (HF_TIMELINE=1 -> libhf_tl.so; HF_ERR_UNSUPPORTED otherwise); n >= 148*16*72 */
 HF_API int hf_timeline_fetch(unsigned long long* host, long long n, int clear);
+/* Launch-sequence graphs: the host mirror records one V-cycle (multigrid.py:309-351: smoothers,
+ * residual, transfers, coarse solve) as a CUDA graph and replays it once per preconditioner
+ * application (multigrid.py:350).  hf_graph_begin starts recording the launches made on `stream`
+ * (not the default stream; no device allocation may happen until hf_graph_end); hf_graph_end
+ * finishes it.  *g == NULL: a new executable graph is created.  *g != NULL (a graph recorded
+ * earlier from a launch sequence of the same shape, e.g. the previous Newton iteration's
+ * hierarchy): it is updated in place (*updated = 1), or re-created if the shapes differ. */
+typedef struct hf_graph hf_graph;
+HF_API int hf_graph_begin(void* stream);
+HF_API int hf_graph_end(void* stream, hf_graph** g, int* updated);
+HF_API int hf_graph_launch(hf_graph* g, void* stream);
+HF_API int hf_graph_destroy(hf_graph* g);
 /* wait for the work queued on `stream` (e.g. after hf_tangent_apply_host) */
 HF_API int hf_stream_synchronize(void* stream);
 /* page-lock / release caller-owned host memory (cudaHostRegister) */

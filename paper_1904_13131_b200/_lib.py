@@ -60,6 +60,10 @@ _SIGS = {
     "hf_tangent_apply_host": (I, [P, P, P, I, P]),
     "hf_host_register": (I, [P, LL]),
     "hf_stream_synchronize": (I, [P]),
+    "hf_graph_begin": (I, [P]),
+    "hf_graph_end": (I, [P, ct.POINTER(P), ct.POINTER(I)]),
+    "hf_graph_launch": (I, [P, P]),
+    "hf_graph_destroy": (I, [P]),
     "hf_timeline_fetch": (I, [P, LL, I]),
     "hf_tangent_host_info": (I, [P, ct.POINTER(I), ct.POINTER(ct.c_float)]),
     "hf_host_unregister": (I, [P]),

@@ -511,14 +511,25 @@ class GMGPreconditioner:
         _v_cycle_into(self.levels, self.transfers, self._b, self._x, len(self.levels) - 1, self.smoothing_steps,
                       self.settings)
 
+    def _record(self):
+        """The V-cycle as one graph.  Recorded through libhf, where the executable
+        graph of an earlier hierarchy of the same shape (levels, strategies,
+        storage, smoothing) is updated in place; HF_GRAPH=torch records with
+        torch.cuda.CUDAGraph instead (a new instantiation per hierarchy)."""
+        if os.environ.get("HF_GRAPH", "native") == "torch":
+            return dv.capture_graph(self._run)
+        key = ("vcycle", torch.cuda.current_device(), self.smoothing_steps, self.settings.degree,
+               tuple((lv.problem.n_dofs, lv.problem.degree, lv.op.strategy, str(lv.b.dtype)) for lv in self.levels))
+        return dv.LaunchGraph(self._run, key)
+
     def apply_into(self, b: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
         self._b.copy_(b)
         if not self.use_graph:
             self._run()
         else:
             if self._graph is None:
-                self._run()  # eager warm-up, then capture the identical launch sequence
-                self._graph = dv.capture_graph(self._run)
+                self._run()  # eager warm-up, then record the identical launch sequence
+                self._graph = self._record()
                 self._b.copy_(b)
             self._graph.replay()
         out.copy_(self._x)
