@@ -244,3 +244,47 @@ def test_coarse_kernel_matches_launches(case, single, monkeypatch):
         its[mode] = cg(op, g["b"], rel_tol=1e-8, preconditioner=gmg)
     assert abs(its["kernel"][1].iterations - its["launches"][1].iterations) <= 1
     assert rel(its["kernel"][0], its["launches"][0]) < 1e-6
+
+
+def test_vcycle_graph_updated_in_place_for_a_rebuilt_hierarchy():
+    """A second hierarchy of the same shape (another linearisation point: new
+    caches, diagonals and Chebyshev coefficients) reuses the first one's
+    executable graph through hf_graph_end's in-place update; its replayed
+    V-cycle equals its own eager run, and the first hierarchy's result is not
+    what it returns."""
+    import gc
+
+    from paper_1904_13131_b200 import build_gmg, build_transfers
+
+    import ctypes as ct
+
+    from paper_1904_13131_b200 import device as dv
+    from paper_1904_13131_b200._lib import lib
+
+    for handles in dv.LaunchGraph._idle.values():  # start without idle graphs from earlier tests
+        for h in handles:
+            lib().hf_graph_destroy(ct.c_void_p(h))
+    dv.LaunchGraph._idle.clear()
+    g = golden("mg_3d_8.npz")
+    probs = product_levels(g)
+    transfers = build_transfers(probs)
+    b = g["b"]
+    first = build_gmg(probs, g["ubar"], "tensor4", seed=0, transfers=transfers)
+    z1 = first.apply(b)
+    assert not first._graph.updated
+    del first
+    gc.collect()
+    u2 = 0.5 * g["ubar"]
+    second = build_gmg(probs, u2, "tensor4", seed=0, transfers=transfers)
+    z2 = second.apply(b)
+    assert second._graph.updated, "the idle executable graph of the same shape was not reused"
+    # the same hierarchy run eagerly (two separately built hierarchies differ by ~1e-7: the coarsest
+    # level's lam_min comes from 120 Lanczos steps without re-orthogonalisation, multigrid.py:231-242)
+    import torch
+
+    second._b.copy_(torch.from_numpy(b).cuda())
+    second._run()
+    ze = second._x.cpu().numpy()
+    assert rel(z2, ze) < 1e-11
+    assert rel(z2, z1) > 1e-6  # a different operator: the update carried the new pointers and coefficients
+    assert rel(second.apply(b), ze) < 1e-11  # replay
