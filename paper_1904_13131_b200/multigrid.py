@@ -529,7 +529,15 @@ class GMGPreconditioner:
         else:
             if self._graph is None:
                 self._run()  # eager warm-up, then record the identical launch sequence
-                self._graph = self._record()
+                try:
+                    self._graph = self._record()
+                except RuntimeError as exc:  # e.g. a device allocation inside the recording
+                    log.warning("V-cycle graph recording failed (%s); running the V-cycle eagerly", exc)
+                    self.use_graph = False
+                    self._b.copy_(b)
+                    self._run()
+                    out.copy_(self._x)
+                    return out
                 self._b.copy_(b)
             self._graph.replay()
         out.copy_(self._x)
