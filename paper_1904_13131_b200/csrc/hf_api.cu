@@ -655,6 +655,19 @@ static int tangent_apply(hf_tangent* op, const double* x_dev, double* y_dev, con
   if (op->alternate && tile1 < 0) {  // whole-range apply: every other sweep backwards
     a.reverse = op->flip;
     op->flip ^= 1;
+  } else if (tile1 < 0) {
+    // Whole-range applies that do not alternate walk the tiles backwards.  The
+    // vector kernels around an apply (Chebyshev and CG updates, dots) stream
+    // their operands forwards, so L2 holds the END of x and y when the apply
+    // starts and the kernel after it starts where the apply's last
+    // reductions landed.  Config-4 CG iteration 10.53 -> 10.39 ms
+    // (profiles/r02/ab_l2_evict_first.txt); HF_REVERSE=0 restores forwards.
+    static int rev = -1;
+    if (rev < 0) {
+      const char* e = std::getenv("HF_REVERSE");
+      rev = e ? std::atoi(e) : 1;
+    }
+    a.reverse = rev;
   }
   HF_CUDA(cell(op->sp, OP_APPLY, op->strategy, a, S(stream)));
   return HF_OK;

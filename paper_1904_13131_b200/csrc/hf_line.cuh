@@ -258,6 +258,31 @@ HF_DEV void last_axis_line(const HfLattice& lat, unsigned node0, int t, unsigned
   nb = node0 + i + (DIM == 3 ? j * sy : 0u);
 }
 
+// The scatter's reductions are evict-last in L2: the kernel after an apply
+// (Chebyshev or CG update, dot) reads y, and the evict-first cache stream
+// leaves room for it.  Config-4 CG iteration with tensor2 8.04 -> 7.95 ms,
+// k_cheb 1.36 -> 1.27 ms per iteration (profiles/r02/ab_l2_evict_first.txt);
+// the same hint on the x gathers moved time from k_cheb into the apply.
+HF_DEV unsigned long long l2_keep_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+HF_DEV void red_keep(double* p, double v, unsigned long long pol) {
+#ifndef HF_NO_L2HINT
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+  atomicAdd(p, v);
+#endif
+}
+HF_DEV void red_keep(float* p, float v, unsigned long long pol) {
+#ifndef HF_NO_L2HINT
+  asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+#else
+  atomicAdd(p, v);
+#endif
+}
+
 // The last-axis line of one tile gathered ahead of use (software pipelining
 // one tile deep): nodal values of x (and ubar for the scalar strategy) and the
 // line's constraint bits (bit c*N + l).
@@ -464,10 +489,25 @@ HF_DEV void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
                : "memory");
 }
 HF_DEV void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+#ifndef HF_NO_L2HINT
+  // The q-point cache is read once per application: its lines are evict-first
+  // in L2, so the stream does not displace the vectors (x gathered ~3.4 times,
+  // y under reduction, the operands of the neighbouring vector kernels).
+  // Measured (profiles/r02/ab_l2_evict_first.txt): tensor4 49.4 vs 50.8 us at
+  // config 2, 37.3 vs 39.4 us at config 3, a config-4 CG iteration -5 %.
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+#endif
 }
 
 // x-derivative at Gauss point iq (a loop variable) of the Gauss-point values q
@@ -857,6 +897,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       c_line<DIM, N, true>(T.V, v);
       unsigned nb, s_last;
       last_axis_line<DIM, N>(a.lat, g.node0, t, nb, s_last);
+      const unsigned long long polk = l2_keep_policy();
 #pragma unroll
       for (int l = 0; l < N; ++l) {
         const unsigned d0 = (nb + l * s_last) * DIM;
@@ -865,7 +906,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
         // no branch per DoF around the reductions
 #pragma unroll
         for (int cc = 0; cc < DIM; ++cc)
-          atomicAdd(reinterpret_cast<ST*>(a.y) + d0 + cc, ((g.mb >> (cc * N + l)) & 1u) ? (ST)0 : (ST)v[cc][l]);
+          red_keep(reinterpret_cast<ST*>(a.y) + d0 + cc, ((g.mb >> (cc * N + l)) & 1u) ? (ST)0 : (ST)v[cc][l], polk);
       }
     }
     __syncwarp();  // line buffers are reused by the next tile
