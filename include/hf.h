@@ -267,6 +267,15 @@ HF_API int hf_cheb_step(long long n, double* x, double* d, const double* b, cons
 HF_API int hf_cheb_step_fill(long long n, double* x, double* d, const double* b, const double* ax, const double* inv_d,
                              int first, double theta, double cd, double cz, int x_zero, const int* skip_dev,
                              const unsigned char* mask, double* y_next, void* stream);
+/* hf_cheb_step (fill_mask == NULL) or hf_cheb_step_fill on fp64 or fp32
+ * vectors (fp_bits), launched as the programmatic dependent of the cell
+ * kernel that wrote ax: the tangent apply of the same smoothing step must be
+ * the launch immediately before on the stream (multigrid.py:195-204).  The
+ * update's blocks load inv_d, b, d and x while that kernel drains and wait for
+ * it before they read ax.  x_zero = 0 and ax != NULL by construction. */
+HF_API int hf_cheb_step_after_apply(long long n, void* x, void* d, const void* b, const void* ax, const void* inv_d,
+                                    int first, double theta, double cd, double cz, const unsigned char* fill_mask,
+                                    void* y_next, int fp_bits, void* stream);
 /* r = b - ax; r[mask] = 0 (v_cycle, multigrid.py:324-325) */
 HF_API int hf_resid_masked(long long n, double* r, const double* b, const double* ax, const unsigned char* mask,
                            void* stream);

@@ -327,6 +327,28 @@ static int transfer_dispatch(hf_transfer* t, bool prolong, const void* in, int i
   return transfer_run(t, prolong, (const float*)in, (float*)out, mode, s);
 }
 
+// hf_cheb_step / hf_cheb_step_fill / hf_cheb_step_f32 launched as the
+// programmatic dependent of the cell kernel that wrote ax (the apply of the
+// same smoothing step, immediately before on the stream)
+template <typename T>
+static cudaError_t launch_cheb_after_apply(long long n, T* x, T* d, const T* b, const T* ax, const T* inv_d, int first,
+                                           double theta, double cd, double cz, const unsigned char* fill_mask,
+                                           T* y_next, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(vec_blocks(n));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int* skip = nullptr;
+  return cudaLaunchKernelEx(&cfg, k_cheb<T>, n, x, d, b, ax, inv_d, first, theta, cd, cz, 0, skip, fill_mask, y_next,
+                            1);
+}
+
 extern "C" {
 
 HF_API const char* hf_last_error(void) { return g_err.c_str(); }
@@ -1395,7 +1417,7 @@ HF_API int hf_cheb_step_f32(long long n, float* x, float* d, const float* b, con
                             const unsigned char* fill_mask, float* y_next, void* stream) {
   if (!x || !d || !b || !inv_d) return fail(HF_ERR_ARG, "null argument");
   k_cheb<float><<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev,
-                                                      fill_mask, y_next);
+                                                      fill_mask, y_next, 0);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }
@@ -1464,7 +1486,7 @@ HF_API int hf_cheb_step(long long n, double* x, double* d, const double* b, cons
                         void* stream) {
   if (!x || !d || !b || !inv_d) return fail(HF_ERR_ARG, "null argument");
   k_cheb<double><<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev,
-                                                       nullptr, nullptr);
+                                                       nullptr, nullptr, 0);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }
@@ -1474,8 +1496,42 @@ HF_API int hf_cheb_step_fill(long long n, double* x, double* d, const double* b,
                              const unsigned char* mask, double* y_next, void* stream) {
   if (!x || !d || !b || !inv_d || !mask || !y_next) return fail(HF_ERR_ARG, "null argument");
   k_cheb<double><<<vec_blocks(n), 256, 0, S(stream)>>>(n, x, d, b, ax, inv_d, first, theta, cd, cz, x_zero, skip_dev,
-                                                       mask, y_next);
+                                                       mask, y_next, 0);
   HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_cheb_step_after_apply(long long n, void* x, void* d, const void* b, const void* ax, const void* inv_d,
+                                    int first, double theta, double cd, double cz, const unsigned char* fill_mask,
+                                    void* y_next, int fp_bits, void* stream) {
+  if (!x || !d || !b || !ax || !inv_d) return fail(HF_ERR_ARG, "null argument");
+  if ((fill_mask == nullptr) != (y_next == nullptr)) return fail(HF_ERR_ARG, "fill_mask and y_next go together");
+  if (fp_bits != 64 && fp_bits != 32) return fail(HF_ERR_ARG, "fp_bits must be 64 or 32");
+  static int pdl = -1;  // HF_PDL_CHEB=0: a plain launch (A/B)
+  if (pdl < 0) {
+    const char* e = std::getenv("HF_PDL_CHEB");
+    pdl = e ? std::atoi(e) : 1;
+  }
+  if (!pdl) {
+    if (fp_bits == 64)
+      k_cheb<double><<<vec_blocks(n), 256, 0, S(stream)>>>(n, (double*)x, (double*)d, (const double*)b,
+                                                           (const double*)ax, (const double*)inv_d, first, theta, cd,
+                                                           cz, 0, nullptr, fill_mask, (double*)y_next, 0);
+    else
+      k_cheb<float><<<vec_blocks(n), 256, 0, S(stream)>>>(n, (float*)x, (float*)d, (const float*)b, (const float*)ax,
+                                                          (const float*)inv_d, first, theta, cd, cz, 0, nullptr,
+                                                          fill_mask, (float*)y_next, 0);
+    HF_CUDA(cudaGetLastError());
+    return HF_OK;
+  }
+  if (fp_bits == 64)
+    HF_CUDA(launch_cheb_after_apply<double>(n, (double*)x, (double*)d, (const double*)b, (const double*)ax,
+                                            (const double*)inv_d, first, theta, cd, cz, fill_mask, (double*)y_next,
+                                            S(stream)));
+  else
+    HF_CUDA(launch_cheb_after_apply<float>(n, (float*)x, (float*)d, (const float*)b, (const float*)ax,
+                                           (const float*)inv_d, first, theta, cd, cz, fill_mask, (float*)y_next,
+                                           S(stream)));
   return HF_OK;
 }
 

@@ -660,6 +660,13 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     if (t_cur >= ntiles) break;
     HF_TL(1 + 4 * (int)k);
     const long long t_nxt = tile_k(k + 1);
+    // A kernel launched as this one's programmatic dependent (the Chebyshev
+    // update of a small level, hf_cheb_step_after_apply) may become resident
+    // once every warp has reached its last tile; it waits for this grid's
+    // completion before it reads y.  Released only after this kernel's own
+    // wait, so that everything before this kernel has completed by then.
+    const bool last = t_nxt >= ntiles;
+    if (last && synced) asm volatile("griddepcontrol.launch_dependents;");
     const ST* cb_nxt = cblock(t_nxt);
     const Gather<DIM, N, VAR> g = nxt;
     gather_tile<DIM, N, VAR, ST>(a, t_nxt, ntiles, m, t, act, nxt);  // in flight during this tile
@@ -889,6 +896,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
     // ---------------- I4: last axis, scatter-add ----------------
     if (!synced) {  // the fill kernel (PDL primary) has completed and its writes are visible
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (last) asm volatile("griddepcontrol.launch_dependents;");
       synced = true;
     }
     if (live) {

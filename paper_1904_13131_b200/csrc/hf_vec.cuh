@@ -150,17 +150,36 @@ __global__ void k_fill_masked(long long n, T* __restrict__ y, const T* __restric
 //   fill_mask != null: also y_next = mask ? x_new : 0, the initialisation of
 //   the NEXT tangent apply (which is launched as this kernel's programmatic
 //   dependent and skips its own fill); y_next may alias ax (read first)
+//   after_apply: this launch is the programmatic dependent of the cell kernel
+//   that wrote ax (hf_cheb_step_after_apply).  Its blocks become resident
+//   while that kernel drains, prefetch into L2 the first operands the cell
+//   kernel does not write (inv_d, b, d, x) and wait for its completion before
+//   they load anything.  The cell kernel releases its dependents after its
+//   own wait, so every kernel before it has completed by then.
 template <typename T = double>
 __global__ void k_cheb(long long n, T* __restrict__ x, T* __restrict__ d, const T* __restrict__ b, const T* ax,
                        const T* __restrict__ inv_d, int first, double theta, double cd, double cz, int x_zero,
-                       const int* skip, const uint8_t* __restrict__ fill_mask, T* y_next) {
+                       const int* skip, const uint8_t* __restrict__ fill_mask, T* y_next, int after_apply) {
   asm volatile("griddepcontrol.launch_dependents;");
+  const long long st = (long long)gridDim.x * blockDim.x;
+  if (after_apply) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x + u * st;
+      if (i < n) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(inv_d + i));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(b + i));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x + i));
+        if (!first) asm volatile("prefetch.global.L2 [%0];" ::"l"(d + i));
+      }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (skip && *skip) return;
   // four elements per thread and iteration with every load issued before any
   // use (one element per iteration left the 64^3 step latency bound at 0.77 of
   // HBM); per element the arithmetic is unchanged, and ax is read before
   // y_next (which may alias it) is written
-  const long long st = (long long)gridDim.x * blockDim.x;
   for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * st) {
     double vb[4], va[4], vi[4], vd[4], vx[4];
     uint8_t vm[4];

@@ -208,6 +208,9 @@ def _cheb_coeffs(lam_max: float, s: ChebyshevSettings):
     return theta, coefs
 
 
+_PDL_CHEB_MAX_DOFS = int(os.environ.get("HF_PDL_CHEB_MAX_DOFS", 1 << 18))
+
+
 def _apply_maybe_filled(apply_fn, x, ax, prefilled: bool, skip=None):
     if prefilled:
         return apply_fn.apply_after_fill(x, ax, skip)
@@ -227,6 +230,13 @@ def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings,
     n = x.numel()
     L = lib()
     fuse = mask is not None and hasattr(apply_fn, "apply_after_fill")
+    # The launch before an update is libhf's cell kernel: on small levels the
+    # update runs as its programmatic dependent (hf_cheb_step_after_apply),
+    # which hides its launch latency: a smoothing at 8^3 49.4 -> 47.3 us, at
+    # 16^3 86.2 -> 84.2 us, the config-1 solve 12.5 -> 11.9 ms.  On large levels
+    # the early-resident update blocks slow the cell kernel (64^3: +3 %), so
+    # those keep the plain launch (profiles/r02/experiments/ab_pdl_cheb.txt).
+    chained = isinstance(apply_fn, MatrixFreeTangent) and n <= _PDL_CHEB_MAX_DOFS
     filled = False
     n_upd = steps * (1 + len(coefs))
     k = 0
@@ -235,6 +245,12 @@ def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings,
         nonlocal filled, k
         k += 1
         fill = fuse and (k < n_upd or fill_last)
+        if chained and not zero:
+            check(L.hf_cheb_step_after_apply(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), dv.ptr(ax), dv.ptr(inv_d), first, th,
+                                             cd, cz, mask if fill else None, dv.ptr(ax) if fill else None, _bits(x),
+                                             dv.stream()))
+            filled = fill
+            return
         args = (n, dv.ptr(x), dv.ptr(d), dv.ptr(b), None if zero else dv.ptr(ax), dv.ptr(inv_d), first, th, cd, cz,
                 int(zero), None)
         if x.dtype == torch.float32:
