@@ -620,7 +620,20 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   // fill is still running: TMA loads, gathers and the evaluation overlap it,
   // and griddepcontrol.wait orders only the first scatter-add after it.
   bool synced = a.fill != 1;
+#ifdef HF_EARLY_XWAIT
+  const bool late_x = false;
   if (a.fill == 2) asm volatile("griddepcontrol.wait;" ::: "memory");  // x comes from the primary
+#else
+  // a.fill == 2: x comes from the primary, but the cache does not.  On small
+  // levels (at most two rounds of tiles) the first TMA chunks and the lane
+  // offsets are issued while the primary still runs and the wait stands only
+  // in front of the first gather: a smoothing at 8^3 47.0 -> 43.2 us, at 16^3
+  // 84.2 -> 82.2 us; at 32^3 the early burst competes with the primary's own
+  // traffic (+0.6 %), so larger launches wait first
+  // (profiles/r02/experiments/ab_pdl_cheb.txt).
+  const bool late_x = a.fill == 2 && (a.tile1 - a.tile0) <= 2ll * W * (long long)gridDim.x;
+  if (a.fill == 2 && !late_x) asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
 
   // Start-up order: the first tile's gather, then its TMA chunks, then the
   // constant-bank offsets.  Every warp of the grid starts at once and the TMA
@@ -631,7 +644,7 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   line_slot<DIM, N>(lane, slot, m, t, act);
   Gather<DIM, N, VAR> nxt;
   long long t_cur = tile_k(0);  // this work item's tile and the next one's
-  gather_tile<DIM, N, VAR, ST>(a, t_cur, ntiles, m, t, act, nxt);
+  if (!late_x) gather_tile<DIM, N, VAR, ST>(a, t_cur, ntiles, m, t, act, nxt);
   HF_TL(HF_TL_SLOTS - 4);
   const ST* cb_cur = cblock(t_cur);
   if (lane == 0) {
@@ -647,6 +660,10 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
   if (lo.off[0][0] == 12345) lbuf[0] = 0;  // the timestamp below waits for the offsets
 #endif
   HF_TL(HF_TL_SLOTS - 2);
+  if (late_x) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    gather_tile<DIM, N, VAR, ST>(a, t_cur, ntiles, m, t, act, nxt);
+  }
   double* wb = lbuf + (size_t)warp * NB * Y::BUF;
   double* bufs[NB];
 #pragma unroll
