@@ -290,6 +290,11 @@ HF_API int hf_cg_update_xr(hf_ws* w, long long n, double* x, double* r, const do
 /* p = z + (scal[irzn]/scal[irz]) p */
 HF_API int hf_cg_update_p(long long n, double* p, const double* z, const double* scal_dev, int irzn, int irz,
                           void* stream);
+/* hf_cg_update_p + the initialisation y_next = mask ? p_new : 0 of the tangent
+ * apply A p that follows (solver.py:58, 73); that apply is then launched with
+ * hf_tangent_apply_after_fill as this kernel's programmatic dependent */
+HF_API int hf_cg_update_p_fill(long long n, double* p, const double* z, const double* scal, int irzn, int irz,
+                               const unsigned char* mask, double* y_next, void* stream);
 /* z = inv_d r; out_dev[0] = r . z */
 HF_API int hf_jacobi_dot(hf_ws* w, long long n, double* z, const double* r, const double* inv_d, double* out_dev,
                          void* stream);

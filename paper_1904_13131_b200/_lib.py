@@ -93,6 +93,7 @@ _SIGS = {
     "hf_scalar_op": (I, [I, P, I, I, D, P, P]),
     "hf_cg_update_xr": (I, [P, LL, P, P, P, P, P, I, I, I, P]),
     "hf_cg_update_p": (I, [LL, P, P, P, I, I, P]),
+    "hf_cg_update_p_fill": (I, [LL, P, P, P, I, I, P, P, P]),
     "hf_jacobi_dot": (I, [P, LL, P, P, P, P, P]),
     "hf_axpby": (I, [LL, D, P, D, P, P]),
     "hf_lanczos_init": (I, [P, P, P]),

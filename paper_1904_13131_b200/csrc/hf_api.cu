@@ -1573,7 +1573,15 @@ HF_API int hf_cg_update_xr(hf_ws* w, long long n, double* x, double* r, const do
 HF_API int hf_cg_update_p(long long n, double* p, const double* z, const double* scal, int irzn, int irz,
                           void* stream) {
   if (!p || !z || !scal) return fail(HF_ERR_ARG, "null argument");
-  k_cg_p<<<vec_blocks(n), 256, 0, S(stream)>>>(n, p, z, scal, irzn, irz);
+  k_cg_p<<<vec_blocks(n), 256, 0, S(stream)>>>(n, p, z, scal, irzn, irz, nullptr, nullptr);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
+HF_API int hf_cg_update_p_fill(long long n, double* p, const double* z, const double* scal, int irzn, int irz,
+                               const unsigned char* mask, double* y_next, void* stream) {
+  if (!p || !z || !scal || !mask || !y_next) return fail(HF_ERR_ARG, "null argument");
+  k_cg_p<<<vec_blocks(n), 256, 0, S(stream)>>>(n, p, z, scal, irzn, irz, mask, y_next);
   HF_CUDA(cudaGetLastError());
   return HF_OK;
 }

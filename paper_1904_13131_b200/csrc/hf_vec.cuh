@@ -260,11 +260,18 @@ __global__ void k_cg_xr(long long n, double* __restrict__ x, double* __restrict_
 }
 
 //   beta = scal[irzn] / scal[irz];  p = z + beta p
+//   fill_mask != null: also y_next = mask ? p_new : 0, the initialisation of
+//   the tangent apply A p that follows (launched as this kernel's programmatic
+//   dependent, hf_tangent_apply_after_fill), as k_cheb does for the smoother
 __global__ void k_cg_p(long long n, double* __restrict__ p, const double* __restrict__ z, const double* scal, int irzn,
-                       int irz) {
+                       int irz, const uint8_t* __restrict__ fill_mask, double* __restrict__ y_next) {
+  asm volatile("griddepcontrol.launch_dependents;");
   const double beta = scal[irzn] / scal[irz];
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    p[i] = z[i] + beta * p[i];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double pn = z[i] + beta * p[i];
+    p[i] = pn;
+    if (fill_mask) y_next[i] = fill_mask[i] ? pn : 0.0;
+  }
 }
 
 // z = inv_d * r; scal[out] = r.z  (Jacobi-preconditioned Lanczos, multigrid.py:126-153)

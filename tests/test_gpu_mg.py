@@ -96,6 +96,28 @@ def test_gmg_cg(case):
     assert np.allclose(h[:k], g["cg_history"][:k], rtol=1e-5)
 
 
+def test_cg_fused_p_update_matches_plain_launches(case):
+    """cg on the tangent itself fuses the p update with the next A p's
+    initialisation and chains that apply as a programmatic dependent
+    (hf_cg_update_p_fill); through a plain ``apply_into`` wrapper it launches
+    the update, the fill and the apply separately.  Same iteration, so the
+    residual histories agree to rounding (the scatter's atomic order)."""
+    from paper_1904_13131_b200 import MatrixFreeTangent, cg
+
+    g, probs, _, gmg = case
+    op = MatrixFreeTangent(probs[-1], g["ubar"], str(g["strategy"]))
+
+    class Plain:
+        def apply_into(self, x, y):
+            return op.apply_into(x, y)
+
+    x1, r1 = cg(op, g["b"], rel_tol=1e-8, preconditioner=gmg)
+    x2, r2 = cg(Plain(), g["b"], rel_tol=1e-8, preconditioner=gmg)
+    assert r1.iterations == r2.iterations
+    assert np.allclose(r1.residual_history, r2.residual_history, rtol=1e-6)
+    assert rel(x1, x2) < 1e-8
+
+
 def test_newton_traction_reference():
     """The reference's own newton_solve (traction) on a tiny 2D problem."""
     from paper_1904_13131_b200 import LoadSpec, NewtonSettings, newton_solve
