@@ -96,6 +96,23 @@ def test_gmg_cg(case):
     assert np.allclose(h[:k], g["cg_history"][:k], rtol=1e-5)
 
 
+def test_chained_chebyshev_update_matches_plain_launch(case, monkeypatch):
+    """On small levels the Chebyshev update is launched as the cell kernel's
+    programmatic dependent (hf_cheb_step_after_apply); with the threshold at
+    zero every update is a plain launch.  Same arithmetic: the smoothed
+    iterates agree to the rounding of the scatter's atomic order."""
+    from paper_1904_13131_b200 import ChebyshevSettings, chebyshev_apply, multigrid
+
+    g, _, _, gmg = case
+    lv = gmg.levels[-1]
+    assert lv.problem.n_dofs <= multigrid._PDL_CHEB_MAX_DOFS
+    chained = chebyshev_apply(lv.op, lv.inv_diag, lv.lam_max, g["b"], g["cheb_x0"], ChebyshevSettings(), 2)
+    monkeypatch.setattr(multigrid, "_PDL_CHEB_MAX_DOFS", 0)
+    plain = chebyshev_apply(lv.op, lv.inv_diag, lv.lam_max, g["b"], g["cheb_x0"], ChebyshevSettings(), 2)
+    assert rel(chained, plain) < 1e-12
+    assert rel(chained, g["cheb_out"]) < 1e-10
+
+
 def test_cg_fused_p_update_matches_plain_launches(case):
     """cg on the tangent itself fuses the p update with the next A p's
     initialisation and chains that apply as a programmatic dependent
