@@ -199,7 +199,12 @@ HF_API int hf_host_unregister(void* host_ptr);
  * backwards, ...): a sweep then starts on the q-point cache tiles the previous
  * one read last, which a 126 MB L2 may still hold.  Off by default (the
  * single-apply benchmark streams the cache); the multigrid levels turn it on
- * for their smoother sweeps.  Results change only by summation order. */
+ * for their smoother sweeps.  Results change only by summation order.
+ * Without it a whole-range apply walks the tiles from the last to the first
+ * (the vector kernels around it stream forwards, so L2 holds the end of x and
+ * y when it starts; environment HF_REVERSE=0 restores forwards).  In either
+ * direction the q-point cache is streamed through L2 evict-first and the
+ * scatter's reductions are evict-last. */
 HF_API int hf_tangent_set_alternate(hf_tangent* op, int on);
 /* matrix-based baseline (assemble_matrix / AssembledTangent, operators.py:436-516):
  * vals_dev (n_el, nld, nld) element matrices of a tensor4 tangent, nld = nloc*dim,
