@@ -823,10 +823,25 @@ __global__ void __launch_bounds__(LinePlan<DIM, N, VAR, ST>::NT, 1)
       static_assert(RW <= N, "a ring at least a tile deep is exactly a tile deep");
       // the whole tile's chunks are resident: wait once, then the N points
       // are free of barriers and the compiler interleaves their chains
+      // tensor4's first tile waits per point: at kernel start every warp's
+      // chunks are in one 24 MB burst that HBM delivers in ~3.7 us, chunk 0 of
+      // every warp first, so the point phase can start on chunk 0 while
+      // chunks 1 and 2 arrive (config 2 back to back 50.3 -> 49.6 us).  Later
+      // tiles find their chunks resident; per-point waits there would only
+      // keep the compiler from interleaving the points' chains.  tensor2 and
+      // scalar chunks are small and gain nothing (+0.5 % with the extra code).
+      if (VAR == TENSOR4 && k == 0) {
 #pragma unroll
-      for (int iq = 0; iq < N; ++iq) mbar_wait(full + iq, (unsigned)k & 1u);  // RW == N: chunk iq sits in stage iq
+        for (int iq = 0; iq < N; ++iq) {
+          mbar_wait(full + iq, 0u);
+          point(iq, ring + (size_t)iq * CH + slot);
+        }
+      } else {
 #pragma unroll
-      for (int iq = 0; iq < N; ++iq) point(iq, ring + (size_t)iq * CH + slot);
+        for (int iq = 0; iq < N; ++iq) mbar_wait(full + iq, (unsigned)k & 1u);  // RW == N: chunk iq sits in stage iq
+#pragma unroll
+        for (int iq = 0; iq < N; ++iq) point(iq, ring + (size_t)iq * CH + slot);
+      }
       __syncwarp();
       if (lane < N) {  // stages consumed by every lane: lanes 0..N-1 refill them with the next tile's chunks
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
