@@ -281,6 +281,16 @@ HF_API int hf_cheb_step_fill(long long n, double* x, double* d, const double* b,
 HF_API int hf_cheb_step_after_apply(long long n, void* x, void* d, const void* b, const void* ax, const void* inv_d,
                                     int first, double theta, double cd, double cz, const unsigned char* fill_mask,
                                     void* y_next, int fp_bits, void* stream);
+/* The Chebyshev step in three-term form (multigrid.py:195-204 with the
+ * direction recovered as d = x_k - x_{k-1} instead of stored):
+ *   z = inv_d (b - ax); d = first ? z/theta : cd (x_k - x_{k-1}) + cz z;
+ *   x_{k+1} = x_k + d, written over x_{k-1} (xo); the caller swaps xk and xo.
+ * xk_zero / xprev_zero: that iterate is zero and not read.  One vector write
+ * less per step than hf_cheb_step.  fill_mask / y_next as hf_cheb_step_fill;
+ * after_apply as hf_cheb_step_after_apply; fp_bits 64 or 32. */
+HF_API int hf_cheb3_step(long long n, const void* xk, void* xo, const void* b, const void* ax, const void* inv_d,
+                         int first, double theta, double cd, double cz, int xk_zero, int xprev_zero,
+                         const unsigned char* fill_mask, void* y_next, int fp_bits, int after_apply, void* stream);
 /* r = b - ax; r[mask] = 0 (v_cycle, multigrid.py:324-325) */
 HF_API int hf_resid_masked(long long n, double* r, const double* b, const double* ax, const unsigned char* mask,
                            void* stream);

@@ -88,6 +88,7 @@ _SIGS = {
     "hf_cheb_step": (I, [LL, P, P, P, P, P, I, D, D, D, I, P, P]),
     "hf_cheb_step_fill": (I, [LL, P, P, P, P, P, I, D, D, D, I, P, P, P, P]),
     "hf_cheb_step_after_apply": (I, [LL, P, P, P, P, P, I, D, D, D, P, P, I, P]),
+    "hf_cheb3_step": (I, [LL, P, P, P, P, P, I, D, D, D, I, I, P, P, I, I, P]),
     "hf_resid_masked": (I, [LL, P, P, P, P, P]),
     "hf_resnorm_check": (I, [P, LL, P, P, P, I, I, P, P]),
     "hf_scalar_op": (I, [I, P, I, I, D, P, P]),

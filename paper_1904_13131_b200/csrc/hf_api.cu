@@ -1501,6 +1501,41 @@ HF_API int hf_cheb_step_fill(long long n, double* x, double* d, const double* b,
   return HF_OK;
 }
 
+HF_API int hf_cheb3_step(long long n, const void* xk, void* xo, const void* b, const void* ax, const void* inv_d,
+                         int first, double theta, double cd, double cz, int xk_zero, int xprev_zero,
+                         const unsigned char* fill_mask, void* y_next, int fp_bits, int after_apply, void* stream) {
+  if (!xk || !xo || !b || !inv_d || xk == xo) return fail(HF_ERR_ARG, "null or aliased argument");
+  if ((fill_mask == nullptr) != (y_next == nullptr)) return fail(HF_ERR_ARG, "fill_mask and y_next go together");
+  if (fp_bits != 64 && fp_bits != 32) return fail(HF_ERR_ARG, "fp_bits must be 64 or 32");
+  if (after_apply && !ax) return fail(HF_ERR_ARG, "after_apply needs ax");
+  static int pdl = -1;  // HF_PDL_CHEB=0: plain launches (A/B)
+  if (pdl < 0) {
+    const char* e = std::getenv("HF_PDL_CHEB");
+    pdl = e ? std::atoi(e) : 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(vec_blocks(n));
+  cfg.blockDim = dim3(256);
+  cfg.stream = S(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  const int chained = (after_apply && pdl) ? 1 : 0;
+  if (chained) {
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  if (fp_bits == 64)
+    HF_CUDA(cudaLaunchKernelEx(&cfg, k_cheb3<double>, n, (const double*)xk, (double*)xo, (const double*)b,
+                               (const double*)ax, (const double*)inv_d, first, theta, cd, cz, xk_zero, xprev_zero,
+                               fill_mask, (double*)y_next, chained));
+  else
+    HF_CUDA(cudaLaunchKernelEx(&cfg, k_cheb3<float>, n, (const float*)xk, (float*)xo, (const float*)b,
+                               (const float*)ax, (const float*)inv_d, first, theta, cd, cz, xk_zero, xprev_zero,
+                               fill_mask, (float*)y_next, chained));
+  return HF_OK;
+}
+
 HF_API int hf_cheb_step_after_apply(long long n, void* x, void* d, const void* b, const void* ax, const void* inv_d,
                                     int first, double theta, double cd, double cz, const unsigned char* fill_mask,
                                     void* y_next, int fp_bits, void* stream) {

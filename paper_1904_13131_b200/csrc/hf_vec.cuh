@@ -208,6 +208,63 @@ __global__ void k_cheb(long long n, T* __restrict__ x, T* __restrict__ d, const 
   }
 }
 
+// Chebyshev step in three-term form: the direction is not stored, it is the
+// difference of the last two iterates, d_{k-1} = x_k - x_{k-1}:
+//   z = inv_d * (b - ax)                     (ax == nullptr -> A x_k = 0)
+//   d = first ? z / theta : cd * (x_k - x_{k-1}) + cz * z
+//   x_{k+1} = x_k + d, written over x_{k-1} (xo); the caller swaps the buffers
+//   xk_zero: x_k = 0 (not read); xprev_zero: x_{k-1} = 0 (not read)
+// One vector write less than k_cheb (57 instead of 65 B per DoF); the iterates
+// agree with the stored-direction form to rounding (x_k - x_{k-1} recovers
+// d_{k-1} to an ulp of x).  fill_mask / y_next / after_apply as in k_cheb.
+template <typename T = double>
+__global__ void k_cheb3(long long n, const T* __restrict__ xk, T* __restrict__ xo, const T* __restrict__ b,
+                        const T* ax, const T* __restrict__ inv_d, int first, double theta, double cd, double cz,
+                        int xk_zero, int xprev_zero, const uint8_t* __restrict__ fill_mask, T* y_next,
+                        int after_apply) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const long long st = (long long)gridDim.x * blockDim.x;
+  if (after_apply) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x + u * st;
+      if (i < n) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(inv_d + i));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(b + i));
+        if (!xk_zero) asm volatile("prefetch.global.L2 [%0];" ::"l"(xk + i));
+        if (!first && !xprev_zero) asm volatile("prefetch.global.L2 [%0];" ::"l"(xo + i));
+      }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  const bool rd_prev = !first && !xprev_zero;
+  for (long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * st) {
+    double vb[4], va[4], vi[4], vp[4], vx[4];
+    uint8_t vm[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * st;
+      const bool in = i < n;
+      vi[u] = in ? (double)inv_d[i] : 0.0;
+      vb[u] = in ? (double)b[i] : 0.0;
+      va[u] = (in && ax) ? (double)ax[i] : 0.0;
+      vp[u] = (in && rd_prev) ? (double)xo[i] : 0.0;
+      vx[u] = (in && !xk_zero) ? (double)xk[i] : 0.0;
+      vm[u] = (in && fill_mask) ? fill_mask[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * st;
+      if (i >= n) break;
+      const double z = vi[u] * (vb[u] - va[u]);
+      const double di = first ? z / theta : cd * (vx[u] - vp[u]) + cz * z;
+      const T xn = (T)(vx[u] + di);
+      xo[i] = xn;
+      if (fill_mask) y_next[i] = vm[u] ? xn : (T)0;
+    }
+  }
+}
+
 // r = b - ax, r[mask] = 0
 template <typename T = double>
 __global__ void k_resid_masked(long long n, T* __restrict__ r, const T* __restrict__ b, const T* __restrict__ ax,

@@ -209,6 +209,7 @@ def _cheb_coeffs(lam_max: float, s: ChebyshevSettings):
 
 
 _PDL_CHEB_MAX_DOFS = int(os.environ.get("HF_PDL_CHEB_MAX_DOFS", 1 << 18))
+_CHEB3 = os.environ.get("HF_CHEB3", "1") != "0"  # three-term Chebyshev updates (hf_cheb3_step)
 
 
 def _apply_maybe_filled(apply_fn, x, ax, prefilled: bool, skip=None):
@@ -225,7 +226,14 @@ def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings,
     Chebyshev update also writes ax = mask ? x : 0 for the next operator
     application, which then runs as its programmatic dependent launch;
     ``fill_last`` does so after the final update too (the V-cycle's residual
-    apply follows the pre-smoother)."""
+    apply follows the pre-smoother).
+
+    The updates run in three-term form (hf_cheb3_step): ``d`` is not the stored
+    direction but the second iterate buffer; each update reads x_k and x_{k-1}
+    and writes x_{k+1} over x_{k-1}, one vector write less than the
+    stored-direction form.  The result ends in ``x`` (copied there after an odd
+    number of updates).  ``HF_CHEB3=0`` keeps the stored direction
+    (hf_cheb_step*)."""
     theta, coefs = _cheb_coeffs(lam_max, s)
     n = x.numel()
     L = lib()
@@ -240,11 +248,21 @@ def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings,
     filled = False
     n_upd = steps * (1 + len(coefs))
     k = 0
+    cur, oth = x, d          # three-term form: x_k and the buffer x_{k+1} goes to
+    prev_zero = False        # x_{k-1} = 0 (the update after one from x = 0)
 
     def update(first, th, cd, cz, zero):
-        nonlocal filled, k
+        nonlocal filled, k, cur, oth, prev_zero
         k += 1
         fill = fuse and (k < n_upd or fill_last)
+        if _CHEB3:
+            check(L.hf_cheb3_step(n, dv.ptr(cur), dv.ptr(oth), dv.ptr(b), None if zero else dv.ptr(ax), dv.ptr(inv_d),
+                                  first, th, cd, cz, int(zero), int(prev_zero), mask if fill else None,
+                                  dv.ptr(ax) if fill else None, _bits(x), int(chained and not zero), dv.stream()))
+            cur, oth = oth, cur
+            prev_zero = zero
+            filled = fill
+            return
         if chained and not zero:
             check(L.hf_cheb_step_after_apply(n, dv.ptr(x), dv.ptr(d), dv.ptr(b), dv.ptr(ax), dv.ptr(inv_d), first, th,
                                              cd, cz, mask if fill else None, dv.ptr(ax) if fill else None, _bits(x),
@@ -264,11 +282,13 @@ def _chebyshev_into(apply_fn, inv_d, lam_max, b, x, d, ax, s: ChebyshevSettings,
     for step in range(steps):
         zero = x_zero and step == 0
         if not zero:
-            _apply_maybe_filled(apply_fn, x, ax, filled)
+            _apply_maybe_filled(apply_fn, cur, ax, filled)
         update(1, theta, 0.0, 0.0, zero)
         for cd, cz in coefs:
-            _apply_maybe_filled(apply_fn, x, ax, filled)
+            _apply_maybe_filled(apply_fn, cur, ax, filled)
             update(0, 0.0, cd, cz, False)
+    if cur is not x:  # an odd number of updates left the result in the second buffer
+        x.copy_(cur)
     return filled
 
 
