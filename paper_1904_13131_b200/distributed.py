@@ -908,18 +908,32 @@ class DistLevel:
         self.r = torch.zeros_like(self.b)
 
     def smooth_into(self, b, x, steps: int, s: ChebyshevSettings, x_zero: bool):
+        """Restarted Chebyshev smoothing in three-term form (multigrid._chebyshev_into):
+        ``self.d`` is the second iterate buffer, every update writes x_{k+1} over
+        x_{k-1}; elementwise, so both copies of an interface DoF stay identical."""
         theta, coefs = _cheb_coeffs(self.lam_max, s)
         n, L = x.numel(), lib()
+        cur, oth = x, self.d
+        prev_zero = False
+
+        def update(first, th, cd, cz, zero):
+            nonlocal cur, oth, prev_zero
+            check(L.hf_cheb3_step(n, dv.ptr(cur), dv.ptr(oth), dv.ptr(b), None if zero else dv.ptr(self.ax),
+                                  dv.ptr(self.inv_diag), first, th, cd, cz, int(zero), int(prev_zero), None, None, 64,
+                                  0, dv.stream()))
+            cur, oth = oth, cur
+            prev_zero = zero
+
         for step in range(steps):
             zero = x_zero and step == 0
             if not zero:
-                self.op.apply_into(x, self.ax)
-            check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(self.d), dv.ptr(b), None if zero else dv.ptr(self.ax),
-                                 dv.ptr(self.inv_diag), 1, theta, 0.0, 0.0, int(zero), None, dv.stream()))
+                self.op.apply_into(cur, self.ax)
+            update(1, theta, 0.0, 0.0, zero)
             for cd, cz in coefs:
-                self.op.apply_into(x, self.ax)
-                check(L.hf_cheb_step(n, dv.ptr(x), dv.ptr(self.d), dv.ptr(b), dv.ptr(self.ax), dv.ptr(self.inv_diag),
-                                     0, 0.0, cd, cz, 0, None, dv.stream()))
+                self.op.apply_into(cur, self.ax)
+                update(0, 0.0, cd, cz, False)
+        if cur is not x:
+            x.copy_(cur)
         return x
 
 
