@@ -59,9 +59,11 @@ def test_prescribed_newton_on_parts_matches_single_gpu(nproc, partition):
     assert np.array_equal(a[:, :2], b[:, :2])
     assert np.all(np.abs(a[:, 3] - b[:, 3]) <= 1)
     assert np.allclose(a[:, 2], b[:, 2], rtol=1e-3, atol=1e-11)
-    # each Newton step's CG stops at rel 1e-6 (solver.py:85): the two paths' final
-    # states agree to the Newton tolerance, not to rounding
-    assert r["u_rel"] < 1e-6
+    # each Newton step's CG stops at rel 1e-6 (solver.py:85) and the iteration at
+    # ||du|| <= 1e-5: the two paths' final states agree to the Newton tolerance,
+    # not to rounding.  Measured 0.2e-7 .. 1.1e-6 run to run (the scatter's
+    # atomic order differs between runs and the truncated CG amplifies it).
+    assert r["u_rel"] < 5e-6
 
 
 def _gpus():
