@@ -357,6 +357,12 @@ HF_API int hf_coarse_clone(const hf_coarse* src, void* stream, hf_coarse** out);
 HF_API int hf_lanczos_init(const double* scal_dev, int* state_dev, void* stream);
 HF_API int hf_lanczos_step(hf_ws* w, long long n, double* r, double* z, double* p, const double* ap,
                            const double* inv_d, double* scal_dev, double* ab_dev, int* state_dev, void* stream);
+/* hf_lanczos_step with the r update, the Jacobi scaling and r.z in one pass
+ * and the p update writing y_next = mask ? p : 0, the initialisation of the
+ * next iteration's application A p (launched with hf_tangent_apply_after_fill) */
+HF_API int hf_lanczos_step_fill(hf_ws* w, long long n, double* r, double* z, double* p, const double* ap,
+                                const double* inv_d, double* scal_dev, double* ab_dev, int* state_dev,
+                                const unsigned char* mask, double* y_next, void* stream);
 /* diagnostic: blocks x threads threads run 8 independent chains of `iters`
  * DFMAs (16 * iters flops per thread) -- the measured fp64 roofline peak */
 HF_API int hf_probe_dfma(long long iters, int blocks, int threads, double* sink_dev, void* stream);

@@ -105,6 +105,7 @@ _SIGS = {
     "hf_coarse_update": (I, [P, P, P]),
     "hf_coarse_clone": (I, [P, P, ct.POINTER(P)]),
     "hf_lanczos_step": (I, [P, LL, P, P, P, P, P, P, P, P, P]),
+    "hf_lanczos_step_fill": (I, [P, LL, P, P, P, P, P, P, P, P, P, P, P]),
     "hf_fill_masked_f32": (I, [LL, P, P, P, D, P]),
     "hf_cheb_step_f32": (I, [LL, P, P, P, P, P, I, D, D, D, I, P, P, P, P]),
     "hf_resid_masked_f32": (I, [LL, P, P, P, P, P]),

@@ -1948,6 +1948,24 @@ HF_API int hf_lanczos_step(hf_ws* w, long long n, double* r, double* z, double* 
   return HF_OK;
 }
 
+// hf_lanczos_step with two passes fused (r update + Jacobi + r.z; p update +
+// the next application's initialisation y_next = mask ? p : 0): the next
+// application is then launched with hf_tangent_apply_after_fill
+HF_API int hf_lanczos_step_fill(hf_ws* w, long long n, double* r, double* z, double* p, const double* ap,
+                                const double* inv_d, double* scal_dev, double* ab_dev, int* state_dev,
+                                const unsigned char* mask, double* y_next, void* stream) {
+  if (!w || !r || !z || !p || !ap || !inv_d || !scal_dev || !ab_dev || !state_dev || !mask || !y_next)
+    return fail(HF_ERR_ARG, "null argument");
+  cudaStream_t s = S(stream);
+  k_dot<<<red_blocks(n), RED_THREADS, 0, s>>>(n, p, ap, w->d_partials, w->d_counter, scal_dev + 1, state_dev);
+  k_lanczos_rz<<<red_blocks(n), RED_THREADS, 0, s>>>(n, r, z, ap, inv_d, scal_dev, state_dev, w->d_partials,
+                                                     w->d_counter);
+  k_lanczos_scalar<<<1, 1, 0, s>>>(scal_dev, state_dev, ab_dev);
+  k_lanczos_p_fill<<<vec_blocks(n), 256, 0, s>>>(n, p, z, scal_dev, state_dev, mask, y_next);
+  HF_CUDA(cudaGetLastError());
+  return HF_OK;
+}
+
 HF_API int hf_axpby(long long n, double a, const double* x, double b, double* y, void* stream) {
   if (!x || !y) return fail(HF_ERR_ARG, "null argument");
   k_axpby<<<vec_blocks(n), 256, 0, S(stream)>>>(n, a, x, b, y);

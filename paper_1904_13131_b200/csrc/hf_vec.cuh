@@ -356,6 +356,25 @@ __global__ void k_lanczos_r(long long n, double* __restrict__ r, const double* _
     r[i] = fma(a, ap[i], r[i]);
 }
 
+// k_lanczos_r and k_jacobi_dot in one pass (same arithmetic per element, same
+// reduction tree as k_jacobi_dot): r -= alpha ap unless the run has stopped,
+// z = inv_d r, scal[2] = r.z
+__global__ void k_lanczos_rz(long long n, double* __restrict__ r, double* __restrict__ z,
+                             const double* __restrict__ ap, const double* __restrict__ inv_d, double* scal,
+                             const int* st, double* partials, unsigned* counter) {
+  const bool upd = !(st[0] || scal[1] <= 0.0);
+  const double a = upd ? -(scal[0] / scal[1]) : 0.0;
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double ri = upd ? fma(a, ap[i], r[i]) : r[i];
+    if (upd) r[i] = ri;
+    const double zi = inv_d[i] * ri;
+    z[i] = zi;
+    s = fma(ri, zi, s);
+  }
+  grid_reduce(s, partials, counter, scal + 2);
+}
+
 // one thread: the reference's tests and recording after r.z (rz_new) is known
 __global__ void k_lanczos_scalar(double* scal, int* st, double* ab) {
   if (st[0]) return;
@@ -385,6 +404,20 @@ __global__ void k_lanczos_p(long long n, double* __restrict__ p, const double* _
   const double b = scal[3];
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     p[i] = fma(b, p[i], z[i]);
+}
+
+// k_lanczos_p that also writes y_next = mask ? p_new : 0, the initialisation of
+// the application A p of the next iteration (its programmatic dependent)
+__global__ void k_lanczos_p_fill(long long n, double* __restrict__ p, const double* __restrict__ z, const double* scal,
+                                 const int* st, const uint8_t* __restrict__ mask, double* __restrict__ y_next) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (st[0]) return;
+  const double b = scal[3];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double pn = fma(b, p[i], z[i]);
+    p[i] = pn;
+    y_next[i] = mask[i] ? pn : 0.0;
+  }
 }
 
 // st[0] = !(rz > 0 and finite), st[1] = 0 (the check before the first iteration)
