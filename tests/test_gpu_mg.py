@@ -113,6 +113,23 @@ def test_chained_chebyshev_update_matches_plain_launch(case, monkeypatch):
     assert rel(chained, g["cheb_out"]) < 1e-10
 
 
+@pytest.mark.parametrize("degree,steps", [(3, 1), (4, 1), (5, 3), (2, 1), (1, 3)])
+def test_three_term_chebyshev_matches_stored_direction(case, degree, steps, monkeypatch):
+    """The product smoother keeps x_{k-1} instead of the direction
+    (hf_cheb3_step, d = x_k - x_{k-1}); hf_cheb_step* store d as the reference
+    does (multigrid.py:195-204).  Same iterates to rounding, for even and odd
+    numbers of updates (an odd count ends in the second buffer and is copied)."""
+    from paper_1904_13131_b200 import ChebyshevSettings, chebyshev_apply, multigrid
+
+    g, _, _, gmg = case
+    lv = gmg.levels[-1]
+    s = ChebyshevSettings(degree=degree)
+    three = chebyshev_apply(lv.op, lv.inv_diag, lv.lam_max, g["b"], g["cheb_x0"], s, steps)
+    monkeypatch.setattr(multigrid, "_CHEB3", False)
+    stored = chebyshev_apply(lv.op, lv.inv_diag, lv.lam_max, g["b"], g["cheb_x0"], s, steps)
+    assert rel(three, stored) < 1e-12
+
+
 def test_cg_fused_p_update_matches_plain_launches(case):
     """cg on the tangent itself fuses the p update with the next A p's
     initialisation and chains that apply as a programmatic dependent
